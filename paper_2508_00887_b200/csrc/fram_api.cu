@@ -1,0 +1,541 @@
+// fram_api.cu — the C ABI of libfram.so (include/fram.h) and the host orchestrator of Alg. 1
+// (PAPER.md P:322-342).  Host code only validates, stages, allocates and sequences kernels; every
+// arithmetic step runs in the CUDA kernels of this library.  One host sync per outer iteration
+// (to read δ and the SDSN pass count); the SDSN pass loop itself is device-resident.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/fram.h"
+#include "internal.h"
+#include "batched.h"
+#include "sharded.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+fram_status fail(fram_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t b) {
+    if (b <= bytes && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) { p = nullptr; return e; }
+    bytes = b;
+    return cudaMemset(p, 0, b);
+  }
+  void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+size_t op_size(int op) { return op == 0 ? 8 : (op == 1 ? 4 : 2); }
+size_t dt_size(int dt) { return dt == 0 ? 8 : (dt == 1 ? 4 : 2); }
+
+}  // namespace
+
+struct fram_ctx {
+  int64_t n = 0;
+  double lambda = 1.0;
+  fram_schedule sched{};
+  std::vector<int32_t> replay;
+  int device = 0;
+  int num_sms = 148;
+  long ld = 0;
+  // workspace
+  DevBuf Aq, BqT, Kq, N, Nq, UT, Y, colpart, Spart, Mpart, cvec, bar, scal, ghist, upd, lapw, permd;
+  DevBuf stA, stB, stK, stX0, stX;
+  DevBuf scan;
+  double* hscal = nullptr;          // pinned readback
+  cudaEvent_t ev[8] = {};
+  int64_t launches = 0;
+  // batched workspace
+  fram::BatchedWs bws;
+  // sharded
+  fram::ShardCtx* shard = nullptr;
+};
+
+namespace {
+
+constexpr int kScalDoubles = 32;     // scal layout: [0..3] sdsn_out, [4..6] upd out3, [8] passes (int)
+
+fram_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) return fail(FRAM_ERR_OOM, std::string(what) + ": out of device memory");
+  return fail(FRAM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(expr, what)                                 \
+  do {                                                 \
+    cudaError_t _e = (expr);                           \
+    if (_e != cudaSuccess) return cuda_fail(_e, what); \
+  } while (0)
+
+fram_status check_schedule(const fram_schedule& s) {
+  if (!(s.theta > 0) || !std::isfinite(s.theta)) return fail(FRAM_ERR_USAGE, "theta must be > 0");
+  if (!(s.alpha > 0 && s.alpha <= 1)) return fail(FRAM_ERR_USAGE, "alpha must be in (0,1]");
+  if (!(s.gamma_th > 0)) return fail(FRAM_ERR_USAGE, "gamma_th must be > 0");
+  if (!(s.delta_th >= 0)) return fail(FRAM_ERR_USAGE, "delta_th must be >= 0");
+  if (s.max_outer < 1 || s.sdsn_max < 1 || s.sdsn_fixed < 0) return fail(FRAM_ERR_USAGE, "bad caps");
+  if (s.replay_len < 0 || (s.replay_len > 0 && !s.replay_passes)) return fail(FRAM_ERR_USAGE, "bad replay");
+  for (int i = 0; i < s.replay_len; ++i)
+    if (s.replay_passes[i] < 1) return fail(FRAM_ERR_USAGE, "replay pass counts must be >= 1");
+  return FRAM_OK;
+}
+
+fram_schedule default_schedule() {
+  fram_schedule s{};
+  s.theta = 10.0;
+  s.alpha = 0.95;
+  s.gamma_th = 1e-3;
+  s.delta_th = 1e-4;
+  s.max_outer = 100;
+  s.sdsn_max = 1000;
+  s.sdsn_fixed = 0;
+  s.flags = FRAM_FLAG_CHECK_SYMMETRY;
+  return s;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Returns a device pointer holding `bytes` of the caller's data (the pointer itself if on device).
+fram_status stage_in(fram_ctx* h, DevBuf& buf, const void* src, size_t bytes, cudaStream_t st, const void** out) {
+  if (!src) { *out = nullptr; return FRAM_OK; }
+  if (is_device_ptr(src)) { *out = src; return FRAM_OK; }
+  CK(buf.ensure(bytes), "staging alloc");
+  CK(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, st), "H2D copy");
+  (void)h;
+  *out = buf.p;
+  return FRAM_OK;
+}
+
+long ld_for(int64_t n) { return (long)((n + 15) / 16 * 16); }
+
+int sdsn_cap(const fram_ctx* h) {
+  int cap = std::max(h->sched.sdsn_max, h->sched.sdsn_fixed);
+  for (int32_t r : h->replay) cap = std::max(cap, r);
+  return cap + 1;
+}
+
+// Allocate the solve workspace for operand format `op`.
+fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
+  const long n = h->n, ld = h->ld;
+  const size_t nn = (size_t)n * ld;
+  const bool f64 = (op == 0);
+  const int G = fram::sdsn_grid_for(n, h->num_sms);
+  CK(h->Aq.ensure(nn * op_size(op)), "alloc A'");
+  CK(h->BqT.ensure(nn * op_size(op)), "alloc B'");
+  if (withK) CK(h->Kq.ensure(nn * (f64 ? 8 : 4)), "alloc K'");
+  CK(h->N.ensure(nn * 8), "alloc N");
+  if (!f64) CK(h->Nq.ensure(nn * op_size(op)), "alloc Nq");
+  CK(h->UT.ensure(nn * op_size(op)), "alloc U");
+  CK(h->Y.ensure(nn * (f64 ? 8 : 4)), "alloc G/Y");
+  CK(h->colpart.ensure((size_t)G * ld * (f64 ? 8 : 4)), "alloc colpart");
+  CK(h->Spart.ensure((size_t)G * 8), "alloc Spart");
+  CK(h->Mpart.ensure((size_t)G * 8), "alloc Mpart");
+  CK(h->cvec.ensure((size_t)ld * 8), "alloc cvec");
+  CK(h->bar.ensure(64), "alloc bar");
+  CK(h->scal.ensure(kScalDoubles * 8), "alloc scal");
+  CK(h->ghist.ensure((size_t)sdsn_cap(h) * 8), "alloc ghist");
+  CK(h->upd.ensure((size_t)(h->num_sms * 4 * 2 + 16) * 8), "alloc upd");
+  CK(h->lapw.ensure(fram::lap_work_bytes(n)), "alloc lap");
+  CK(h->permd.ensure((size_t)n * 4), "alloc perm");
+  CK(h->scan.ensure(sizeof(fram::PrecondScan)), "alloc scan");
+  if (!h->hscal) CK(cudaMallocHost((void**)&h->hscal, kScalDoubles * 8), "alloc pinned");
+  for (auto& e : h->ev)
+    if (!e) CK(cudaEventCreate(&e), "event create");
+  return FRAM_OK;
+}
+
+fram_status set_device(fram_ctx* h) {
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  if (e != cudaSuccess || cnt == 0) return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "no CUDA device");
+  CK(cudaSetDevice(h->device), "cudaSetDevice");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, h->device), "device properties");
+  if (prop.major != 10) return fail(FRAM_ERR_CUDA, "libfram is built for sm_100a (B200); device is sm_" +
+                                                       std::to_string(prop.major) + std::to_string(prop.minor));
+  h->num_sms = prop.multiProcessorCount;
+  return FRAM_OK;
+}
+
+// Preconditioning (K1): scan → host check → apply.  Returns c in *c_out.
+fram_status precondition(fram_ctx* h, int dt, const void* A, const void* B, const void* K, int op, cudaStream_t st,
+                         double* c_out) {
+  const long n = h->n;
+  fram::PrecondScan* sc = h->scan.as<fram::PrecondScan>();
+  const bool sym = (h->sched.flags & FRAM_FLAG_CHECK_SYMMETRY) != 0;
+  CK(fram::launch_precond_scan(A, B, K, dt, n, sym, sc, nullptr, nullptr, st), "precond scan");
+  h->launches++;
+  fram::PrecondScan hs;
+  CK(cudaMemcpyAsync(&hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, st), "scan readback");
+  CK(cudaStreamSynchronize(st), "scan sync");
+  if (hs.bad_nonfinite) return fail(FRAM_ERR_DATA, "non-finite entries in A, B or K");
+  if (hs.bad_negative) return fail(FRAM_ERR_DATA, "negative entries in A, B or K (P:55)");
+  if (hs.bad_asym) return fail(FRAM_ERR_DATA, "A or B is not symmetric (P:55, R28)");
+  const double c = std::max(std::max(hs.maxv[0], hs.maxv[1]), hs.maxv[2]);
+  if (!(c > 0)) return fail(FRAM_ERR_DATA, "c = max(A, B, K) = 0 (S:344)");
+  if (c_out) *c_out = c;
+  CK(fram::launch_precond_apply(A, B, K, dt, n, h->ld, sc->maxv, op, h->Aq.p, h->BqT.p, K ? h->Kq.p : nullptr,
+                                op == 0, st),
+     "precond apply");
+  h->launches++;
+  return FRAM_OK;
+}
+
+fram_status gradient(fram_ctx* h, int op, bool haveK, cudaStream_t st) {
+  const long n = h->n, ld = h->ld;
+  fram::GemmArgs g1{op == 0 ? h->N.p : h->Nq.p, h->BqT.p, n, n, n, ld, 0, h->UT.p, ld, nullptr, 0.0};
+  fram::GemmArgs g2{h->Aq.p, h->UT.p, n, n, n, ld, 1, h->Y.p, ld, haveK ? h->Kq.p : nullptr, h->lambda};
+  if (op == 0) {
+    CK(fram::launch_gemm_f64(g1, st), "gemm1 f64");
+    CK(fram::launch_gemm_f64(g2, st), "gemm2 f64");
+  } else {
+    CK(fram::launch_gemm_tc(g1, op, st), "gemm1 tcgen05");
+    CK(fram::launch_gemm_tc(g2, op, st), "gemm2 tcgen05");
+  }
+  h->launches += 2;
+  return FRAM_OK;
+}
+
+fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
+  fram::SdsnParams p{};
+  p.Y = h->Y.p;
+  p.n = h->n;
+  p.ld = h->ld;
+  p.theta = h->sched.theta;
+  p.gamma_th = h->sched.gamma_th;
+  p.sdsn_max = h->sched.sdsn_max;
+  p.sdsn_fixed = fixed;
+  p.scale = (h->sched.flags & FRAM_FLAG_NO_THETA_SCALE) ? 0 : 1;
+  p.colpart = h->colpart.p;
+  p.Spart = h->Spart.as<double>();
+  p.Mpart = h->Mpart.as<double>();
+  p.cvec = h->cvec.as<double>();
+  p.bar = h->bar.as<unsigned>();
+  double* scal = h->scal.as<double>();
+  p.passes_out = reinterpret_cast<int*>(scal + 8);
+  p.gamma_hist = h->ghist.as<double>();
+  p.sdsn_out = scal;
+  CK(fram::launch_sdsn(p, f64, st, h->num_sms, nullptr), "sdsn launch");
+  h->launches += 2;   // barrier memset + kernel
+  return FRAM_OK;
+}
+
+int prec_to_op(fram_precision p) { return (int)p; }   // 0 f64, 1 tf32, 2 bf16, 3 fp16
+
+fram_status common_checks(fram_ctx* h, int dt, fram_precision p) {
+  if (!h) return fail(FRAM_ERR_USAGE, "null handle");
+  if (dt < 0 || dt > 2) return fail(FRAM_ERR_USAGE, "bad dtype");
+  if ((int)p < 0 || (int)p > 3) return fail(FRAM_ERR_USAGE, "bad precision");
+  if (h->shard) return fail(FRAM_ERR_USAGE, "use the sharded entry points for a sharded handle");
+  return set_device(h);
+}
+
+}  // namespace
+
+extern "C" {
+
+fram_status fram_create(int64_t n, double lambda, const fram_schedule* s, int device, fram_handle* out) {
+  if (!out) return fail(FRAM_ERR_USAGE, "null out");
+  *out = nullptr;
+  if (n < 1) return fail(FRAM_ERR_USAGE, "n must be >= 1");
+  if (!(lambda >= 0) || !std::isfinite(lambda)) return fail(FRAM_ERR_USAGE, "lambda must be >= 0");
+  fram_schedule sc = s ? *s : default_schedule();
+  fram_status st = check_schedule(sc);
+  if (st != FRAM_OK) return st;
+  fram_ctx* h = new fram_ctx();
+  h->n = n;
+  h->lambda = lambda;
+  h->device = device;
+  h->ld = ld_for(n);
+  h->replay.assign(sc.replay_passes, sc.replay_passes + sc.replay_len);
+  h->sched = sc;
+  h->sched.replay_passes = h->replay.empty() ? nullptr : h->replay.data();
+  *out = h;
+  return FRAM_OK;
+}
+
+fram_status fram_set_schedule(fram_handle h, const fram_schedule* s) {
+  if (!h || !s) return fail(FRAM_ERR_USAGE, "null argument");
+  fram_status st = check_schedule(*s);
+  if (st != FRAM_OK) return st;
+  h->replay.assign(s->replay_passes, s->replay_passes + s->replay_len);
+  h->sched = *s;
+  h->sched.replay_passes = h->replay.empty() ? nullptr : h->replay.data();
+  return FRAM_OK;
+}
+
+void fram_destroy(fram_handle h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  DevBuf* bufs[] = {&h->Aq, &h->BqT, &h->Kq, &h->N, &h->Nq, &h->UT, &h->Y, &h->colpart, &h->Spart, &h->Mpart,
+                    &h->cvec, &h->bar, &h->scal, &h->ghist, &h->upd, &h->lapw, &h->permd, &h->stA, &h->stB,
+                    &h->stK, &h->stX0, &h->stX, &h->scan};
+  for (DevBuf* b : bufs) b->release();
+  if (h->hscal) cudaFreeHost(h->hscal);
+  for (auto& e : h->ev)
+    if (e) cudaEventDestroy(e);
+  fram::batched_release(h->bws);
+  if (h->shard) fram::shard_destroy(h->shard);
+  delete h;
+}
+
+const char* fram_last_error(void) { return g_err.c_str(); }
+int fram_abi_version(void) { return FRAM_ABI_VERSION; }
+const char* fram_build_info(void) { return "libfram sm_100a (tcgen05/TMEM/TMA GEMM, persistent SDSN, DMMA FP64, GPU Hungarian)"; }
+
+fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* B, const void* K, const double* X0,
+                       fram_precision p, void* stream, double* X_out, int32_t* perm_out, fram_stats* stats) {
+  fram_status s0 = common_checks(h, (int)dt, p);
+  if (s0 != FRAM_OK) return s0;
+  if (!A || !B) return fail(FRAM_ERR_USAGE, "A and B are required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int op = prec_to_op(p);
+  const bool f64 = (op == 0);
+  const long n = h->n, ld = h->ld;
+  if (!fram::sdsn_supported(n, f64)) return fail(FRAM_ERR_USAGE, "n too large for the SDSN kernel");
+  h->launches = 0;
+  const bool timing = (h->sched.flags & FRAM_FLAG_TIME_PHASES) != 0;
+  fram_status rs = ensure_ws(h, op, K != nullptr);
+  if (rs != FRAM_OK) return rs;
+  if (timing) CK(cudaEventRecord(h->ev[0], st), "event");
+
+  const size_t in_bytes = (size_t)n * n * dt_size(dt);
+  const void *dA, *dB, *dK, *dX0;
+  if ((rs = stage_in(h, h->stA, A, in_bytes, st, &dA)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stB, B, in_bytes, st, &dB)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stK, K, in_bytes, st, &dK)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stX0, X0, (size_t)n * n * 8, st, &dX0)) != FRAM_OK) return rs;
+
+  double c = 0;
+  if ((rs = precondition(h, (int)dt, dA, dB, dK, op, st, &c)) != FRAM_OK) return rs;
+  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dX0, n, ld, st), "init N");
+  h->launches++;
+  if (timing) CK(cudaEventRecord(h->ev[1], st), "event");
+
+  const fram_schedule& sc = h->sched;
+  const bool replay = !h->replay.empty();
+  const int T = replay ? (int)h->replay.size() : sc.max_outer;
+  double* scal = h->scal.as<double>();
+  double ms_gemm = 0, ms_sdsn = 0, ms_update = 0;
+  int t = 0, capped = 0;
+  int64_t total = 0;
+  bool converged = false;
+  for (t = 1; t <= T; ++t) {
+    if (timing) CK(cudaEventRecord(h->ev[2], st), "event");
+    if ((rs = gradient(h, op, dK != nullptr, st)) != FRAM_OK) return rs;
+    if (timing) CK(cudaEventRecord(h->ev[3], st), "event");
+    const int fixed = replay ? h->replay[t - 1] : sc.sdsn_fixed;
+    if ((rs = run_sdsn(h, f64, fixed, st)) != FRAM_OK) return rs;
+    if (timing) CK(cudaEventRecord(h->ev[4], st), "event");
+    CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, n, ld, sc.alpha, h->upd.as<double>(),
+                           reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8), scal + 4, st,
+                           h->num_sms),
+       "update");
+    h->launches++;
+    if (timing) CK(cudaEventRecord(h->ev[5], st), "event");
+    CK(cudaMemcpyAsync(h->hscal, scal, kScalDoubles * 8, cudaMemcpyDeviceToHost, st), "scalar readback");
+    CK(cudaStreamSynchronize(st), "iteration sync");
+    const int passes = *reinterpret_cast<int*>(h->hscal + 8);
+    const double gam = h->hscal[0];
+    const double delta = h->hscal[6];
+    if (!std::isfinite(delta)) return fail(FRAM_ERR_DATA, "non-finite delta (overflow in the gradient?)");
+    total += passes;
+    if (fixed == 0 && passes >= sc.sdsn_max) ++capped;
+    if (timing) {
+      float a, b, cc;
+      cudaEventElapsedTime(&a, h->ev[2], h->ev[3]);
+      cudaEventElapsedTime(&b, h->ev[3], h->ev[4]);
+      cudaEventElapsedTime(&cc, h->ev[4], h->ev[5]);
+      ms_gemm += a;
+      ms_sdsn += b;
+      ms_update += cc;
+    }
+    if (stats && (sc.flags & FRAM_FLAG_TRACE)) {
+      if (stats->passes_per_iter) stats->passes_per_iter[t - 1] = passes;
+      if (stats->delta_trace) stats->delta_trace[t - 1] = delta;
+      if (stats->gamma_last) stats->gamma_last[t - 1] = gam;
+    }
+    if (delta <= sc.delta_th) {
+      converged = true;
+      if (!replay) break;
+    } else if (replay) {
+      converged = false;
+    }
+  }
+  if (t > T) t = T;
+  if (timing) CK(cudaEventRecord(h->ev[6], st), "event");
+  CK(fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
+  h->launches++;
+  if (timing) CK(cudaEventRecord(h->ev[7], st), "event");
+  if (X_out) CK(cudaMemcpy2DAsync(X_out, n * 8, h->N.p, ld * 8, n * 8, n, cudaMemcpyDefault, st), "X_out copy");
+  if (perm_out) CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
+  CK(cudaStreamSynchronize(st), "final sync");
+  if (stats) {
+    stats->outer_iters = t;
+    stats->converged = converged ? 1 : 0;
+    stats->sdsn_capped_calls = capped;
+    stats->total_passes = total;
+    stats->kernel_launches = h->launches;
+    if (timing) {
+      float a, b, cc;
+      cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);
+      cudaEventElapsedTime(&b, h->ev[6], h->ev[7]);
+      cudaEventElapsedTime(&cc, h->ev[0], h->ev[7]);
+      stats->ms_precond = a;
+      stats->ms_lap = b;
+      stats->ms_total = cc;
+      stats->ms_gemm = ms_gemm;
+      stats->ms_sdsn = ms_sdsn;
+      stats->ms_update = ms_update;
+    }
+  }
+  (void)c;
+  if (!converged) {
+    g_err = "max_outer reached without delta <= delta_th";
+    return FRAM_NOT_CONVERGED;
+  }
+  return FRAM_OK;
+}
+
+fram_status fram_sdsn(fram_handle h, fram_precision p, const void* X, void* D_out, int32_t* passes,
+                      double* gamma_hist, void* stream) {
+  fram_status s0 = common_checks(h, 0, p);
+  if (s0 != FRAM_OK) return s0;
+  if (!X || !D_out || !passes) return fail(FRAM_ERR_USAGE, "X, D_out and passes are required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const bool f64 = (p == FRAM_PREC_FP64);
+  const long n = h->n, ld = h->ld;
+  if (!fram::sdsn_supported(n, f64)) return fail(FRAM_ERR_USAGE, "n too large for the SDSN kernel");
+  h->launches = 0;
+  fram_status rs = ensure_ws(h, f64 ? 0 : 1, false);
+  if (rs != FRAM_OK) return rs;
+  const size_t es = f64 ? 8 : 4;
+  const void* dX;
+  if ((rs = stage_in(h, h->stX, X, (size_t)n * n * es, st, &dX)) != FRAM_OK) return rs;
+  unsigned long long* bad = reinterpret_cast<unsigned long long*>(h->scan.p);
+  CK(fram::launch_scan_nonneg(dX, f64, n, bad, st), "scan");
+  unsigned long long hbad = 0;
+  CK(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st), "scan readback");
+  CK(cudaStreamSynchronize(st), "scan sync");
+  if (hbad) return fail(FRAM_ERR_DATA, "SDSN input must be finite and nonnegative (S:251)");
+  CK(cudaMemcpy2DAsync(h->Y.p, ld * es, dX, n * es, n * es, n, cudaMemcpyDeviceToDevice, st), "X copy");
+  if ((rs = run_sdsn(h, f64, h->sched.sdsn_fixed, st)) != FRAM_OK) return rs;
+  CK(cudaMemcpyAsync(h->hscal, h->scal.p, kScalDoubles * 8, cudaMemcpyDeviceToHost, st), "readback");
+  CK(cudaMemcpy2DAsync(D_out, n * es, h->Y.p, ld * es, n * es, n, cudaMemcpyDefault, st), "D copy");
+  CK(cudaStreamSynchronize(st), "sync");
+  const int k = *reinterpret_cast<int*>(h->hscal + 8);
+  *passes = k;
+  if (gamma_hist && k > 0)
+    CK(cudaMemcpy(gamma_hist, h->ghist.p, (size_t)k * 8, cudaMemcpyDeviceToHost), "gamma readback");
+  return FRAM_OK;
+}
+
+fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, const void* B, const void* K,
+                          const double* Nin, fram_precision p, void* stream, void* G_out, double* c_out) {
+  fram_status s0 = common_checks(h, (int)dt, p);
+  if (s0 != FRAM_OK) return s0;
+  if (!A || !B || !Nin || !G_out) return fail(FRAM_ERR_USAGE, "A, B, N and G_out are required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int op = prec_to_op(p);
+  const long n = h->n, ld = h->ld;
+  h->launches = 0;
+  fram_status rs = ensure_ws(h, op, K != nullptr);
+  if (rs != FRAM_OK) return rs;
+  const size_t in_bytes = (size_t)n * n * dt_size(dt);
+  const void *dA, *dB, *dK, *dN;
+  if ((rs = stage_in(h, h->stA, A, in_bytes, st, &dA)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stB, B, in_bytes, st, &dB)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stK, K, in_bytes, st, &dK)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stX0, Nin, (size_t)n * n * 8, st, &dN)) != FRAM_OK) return rs;
+  double c = 0;
+  if ((rs = precondition(h, (int)dt, dA, dB, dK, op, st, &c)) != FRAM_OK) return rs;
+  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dN, n, ld, st), "init N");
+  if ((rs = gradient(h, op, dK != nullptr, st)) != FRAM_OK) return rs;
+  const size_t es = op == 0 ? 8 : 4;
+  CK(cudaMemcpy2DAsync(G_out, n * es, h->Y.p, ld * es, n * es, n, cudaMemcpyDefault, st), "G copy");
+  CK(cudaStreamSynchronize(st), "sync");
+  if (c_out) *c_out = c;
+  return FRAM_OK;
+}
+
+fram_status fram_lap(fram_handle h, const double* Nin, int32_t* perm_out, void* stream) {
+  fram_status s0 = common_checks(h, 0, FRAM_PREC_FP64);
+  if (s0 != FRAM_OK) return s0;
+  if (!Nin || !perm_out) return fail(FRAM_ERR_USAGE, "N and perm_out are required");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const long n = h->n, ld = h->ld;
+  CK(h->N.ensure((size_t)n * ld * 8), "alloc N");
+  CK(h->lapw.ensure(fram::lap_work_bytes(n)), "alloc lap");
+  CK(h->permd.ensure((size_t)n * 4), "alloc perm");
+  CK(cudaMemcpy2DAsync(h->N.p, ld * 8, Nin, n * 8, n * 8, n, cudaMemcpyDefault, st), "N copy");
+  CK(fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
+  CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
+  CK(cudaStreamSynchronize(st), "sync");
+  return FRAM_OK;
+}
+
+fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype dt, const void* A, const void* B,
+                               const void* K, const double* X0, fram_precision p, void* stream, double* X_out,
+                               int32_t* perm_out, int32_t* status_out, fram_stats* stats) {
+  fram_status s0 = common_checks(h, (int)dt, p);
+  if (s0 != FRAM_OK) return s0;
+  if (batch < 0 || !A || !B) return fail(FRAM_ERR_USAGE, "bad batch arguments");
+  std::string err;
+  fram_status s = fram::batched_solve(h->bws, h->n, h->lambda, h->sched, batch, (int)dt, A, B, K, X0, (int)p,
+                                      reinterpret_cast<cudaStream_t>(stream), X_out, perm_out, status_out, stats,
+                                      h->num_sms, &err);
+  if (s != FRAM_OK) g_err = err;
+  return s;
+}
+
+fram_status fram_get_unique_id(uint8_t id[128]) {
+  std::string err;
+  fram_status s = fram::shard_unique_id(id, &err);
+  if (s != FRAM_OK) g_err = err;
+  return s;
+}
+
+fram_status fram_create_sharded(int64_t n, double lambda, const fram_schedule* s, const uint8_t id[128], int rank,
+                                int world, int device, fram_handle* out) {
+  if (!out || !id) return fail(FRAM_ERR_USAGE, "null argument");
+  if (world < 1 || rank < 0 || rank >= world) return fail(FRAM_ERR_USAGE, "bad rank/world");
+  if (n % world != 0) return fail(FRAM_ERR_USAGE, "n % world != 0");
+  fram_status st = fram_create(n, lambda, s, device, out);
+  if (st != FRAM_OK) return st;
+  std::string err;
+  fram_handle h = *out;
+  st = set_device(h);
+  if (st == FRAM_OK) st = fram::shard_create(&h->shard, id, rank, world, &err);
+  if (st != FRAM_OK) {
+    if (!err.empty()) g_err = err;
+    fram_destroy(h);
+    *out = nullptr;
+  }
+  return st;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// gemm_f64.cu — K2d/K3d: the gradient GEMMs in FP64 mode (all steps FP64: the paper's "GPU-FP64"
+// comparison).  tcgen05 has no f64 kind, so this uses the FP64 tensor path through
+// mma.sync.m8n8k4.f64 (DMMA), with cp.async double-buffered SMEM staging.
+// Same NT contract and epilogues as gemm_tc.cu: D = Aop·Bopᵀ; epi 0 stores Dᵀ, epi 1 stores
+// G = D + λK' (FP64).
+#include "common.cuh"
+#include "internal.h"
+
+namespace fram {
+namespace {
+
+constexpr int TM = 64, TN = 64, TK = 16, PADK = TK + 2, THREADS = 128;
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d[0]), "+d"(d[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(THREADS) gemm_f64_kernel(const double* __restrict__ A, const double* __restrict__ B,
+                                                           long M, long N, long K, long ld, int epi, double* out,
+                                                           long ldo, const double* Kq, double lam) {
+  __shared__ __align__(16) double As[2][TM][PADK];
+  __shared__ __align__(16) double Bs[2][TN][PADK];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const long m0 = (long)blockIdx.y * TM, n0 = (long)blockIdx.x * TN;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  auto load_stage = [&](int buf, long k0) {
+    // A tile TM×TK = 64×16 doubles = 512 × 16B chunks; 4 per thread (same for B)
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int c = tid + t * THREADS;
+      const int r = c >> 3, kc = (c & 7) * 2;
+      const long gr = m0 + r, gk = k0 + kc;
+      const bool ok = gr < M && gk < K;
+      cp_async16(&As[buf][r][kc], ok ? (const void*)(A + gr * ld + gk) : (const void*)A, ok);
+      const long gn = n0 + r;
+      const bool okb = gn < N && gk < K;
+      cp_async16(&Bs[buf][r][kc], okb ? (const void*)(B + gn * ld + gk) : (const void*)B, okb);
+    }
+    cp_commit();
+  };
+
+  const int nk = (int)((K + TK - 1) / TK);
+  load_stage(0, 0);
+  for (int kb = 0; kb < nk; ++kb) {
+    const int buf = kb & 1;
+    if (kb + 1 < nk) { load_stage(buf ^ 1, (long)(kb + 1) * TK); cp_wait1(); }
+    else cp_wait0();
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < TK; kk += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][wm + i * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][wn + j * 8 + (lane >> 2)][kk + (lane & 3)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+    __syncthreads();
+  }
+  // epilogue: acc[i][j][e] = D[m0+wm+i*8+lane/4][n0+wn+j*8+2*(lane%4)+e]
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const long r = m0 + wm + i * 8 + (lane >> 2);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const long c = n0 + wn + j * 8 + 2 * (lane & 3) + e;
+        if (r < M && c < N) {
+          if (epi == 0) out[c * ldo + r] = acc[i][j][e];
+          else out[r * ldo + c] = Kq ? acc[i][j][e] + lam * Kq[r * ldo + c] : acc[i][j][e];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_gemm_f64(const GemmArgs& g, cudaStream_t st) {
+  dim3 grid((unsigned)((g.N + TN - 1) / TN), (unsigned)((g.M + TM - 1) / TM));
+  gemm_f64_kernel<<<grid, THREADS, 0, st>>>((const double*)g.Aop, (const double*)g.Bop, g.M, g.N, g.K, g.ld, g.epi,
+                                            (double*)g.out, g.ldo, (const double*)g.Kq, g.lam);
+  return cudaGetLastError();
+}
+
+}  // namespace fram

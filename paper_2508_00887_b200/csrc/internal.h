@@ -1,0 +1,71 @@
+// internal.h — host-side launchers shared between the libfram translation units (not ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fram {
+
+// ---- K4: SDSN (Alg. 2), persistent cooperative kernel, one launch per SDSN call ----
+struct SdsnParams {
+  void* Y;             // n×ld, T = float (mixed) or double (FP64); in: X (G), out: D, in place
+  long n, ld;
+  double theta, gamma_th;
+  int sdsn_max, sdsn_fixed, scale;   // scale = 0 ⇒ skip Alg.2 step 1 (DSPFP)
+  void* colpart;       // [grid][ld] T   per-CTA column partials
+  double* Spart;       // [grid]         per-CTA Σ of its row sums
+  double* Mpart;       // [grid]         per-CTA max
+  double* cvec;        // [ld]           column sums c (FP64)
+  unsigned* bar;       // [2]            grid barrier (zeroed before launch)
+  int* passes_out;     // [1]
+  double* gamma_hist;  // [sdsn_max] nullable: γ_j of every pass input
+  double* sdsn_out;    // [4]: [0] γ of the last pass input, [1] max X, [2] S of last input
+};
+// f64: T=double; else T=float.  Returns the grid used via *grid_out.
+cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_sms, int* grid_out);
+int sdsn_grid_for(long n, int num_sms);
+bool sdsn_supported(long n, bool f64);
+
+// ---- K1: preconditioning (Alg.1 steps 2-3) ------------------------------------
+// in_dt: 0 f64, 1 f32, 2 bf16.  op: 0 f64, 1 tf32 (stored f32), 2 bf16, 3 fp16.
+struct PrecondScan {        // device-side result of the validation / max scan
+  double maxv[3];           // max A, max B, max K
+  unsigned long long bad_nonfinite, bad_negative, bad_asym;
+};
+cudaError_t launch_precond_scan(const void* A, const void* B, const void* K, int in_dt, long n,
+                                bool check_sym, PrecondScan* out_dev, double* blockbuf,
+                                unsigned* counter, cudaStream_t st);
+// A' = A/√c → op (row-major, ld), Bt' = (Ã/√c)ᵀ → op (row-major, ld), K' = K/c → kdst (f32 or f64)
+cudaError_t launch_precond_apply(const void* A, const void* B, const void* K, int in_dt, long n,
+                                 long ld, const double* c_dev, int op, void* Aq, void* BqT,
+                                 void* Kq, bool k_f64, cudaStream_t st);
+
+// ---- K2/K3: gradient GEMMs ------------------------------------------------------------------
+// D[M×N] = Aop[M×K] · Bop[N×K]ᵀ (both row-major, K contiguous, leading dim ld).
+// epi 0: OutT[j*ldo + i] = round_op(D[i][j])  (transposed store in the operand format)
+// epi 1: G[i*ldo + j] = D[i][j] + lam*Kq[i*ldo + j]  (FP32 G; Kq nullable)
+struct GemmArgs {
+  const void* Aop; const void* Bop; long M, N, K, ld;
+  int epi; void* out; long ldo; const void* Kq; double lam;
+};
+cudaError_t launch_gemm_tc(const GemmArgs& g, int op, cudaStream_t st);     // tcgen05 (op 1,2,3)
+cudaError_t launch_gemm_f64(const GemmArgs& g, cudaStream_t st);            // DMMA FP64
+
+// ---- K5/K6: update N ← (1−α)N + αD, N_q, δ (Alg.1 steps 7-8) --------------------------------
+cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long n, long ld,
+                          double alpha, double* partials, unsigned* counter, double* out3,
+                          cudaStream_t st, int num_sms);
+cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long n, long ld,
+                          cudaStream_t st);
+
+// ---- K7: LAP (Alg.1 step 10, R17) --------------------------------------------------------------
+cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* work,
+                       cudaStream_t st);
+size_t lap_work_bytes(long n);
+
+// ---- misc ---------------------------------------------------------------------------------------
+cudaError_t launch_copy2d_f64(double* dst, long ldd, const double* src, long lds, long rows,
+                              long cols, cudaStream_t st);
+cudaError_t launch_scan_nonneg(const void* X, bool f64, long n, unsigned long long* bad,
+                               cudaStream_t st);
+
+}  // namespace fram

@@ -1,0 +1,130 @@
+// update.cu — K5/K6: FRAM update and outer stopping test (Alg.1 steps 7-8).
+//   N⁽ᵗ⁾ = (1−α)N⁽ᵗ⁻¹⁾ + αD⁽ᵗ⁾  (FP64, evaluated unfused as in R15: __dmul_rn/__dadd_rn)
+//   δ⁽ᵗ⁾ = ‖N⁽ᵗ⁾ − N⁽ᵗ⁻¹⁾‖_F / ‖N⁽ᵗ⁾‖_F  (R14)
+// plus N_q = N rounded to the GEMM operand format for the next gradient.  The two sums of squares
+// are reduced deterministically: per-CTA partials, then the last CTA to finish sums them in CTA
+// order and writes out3 = {ΣΔ², ΣN², δ}.
+#include "common.cuh"
+#include "internal.h"
+
+namespace fram {
+namespace {
+
+constexpr int UPD_THREADS = 512;
+
+template <int OP> __device__ __forceinline__ void store_op(void* p, long idx, double v);
+template <> __device__ __forceinline__ void store_op<0>(void*, long, double) {}
+template <> __device__ __forceinline__ void store_op<1>(void* p, long idx, double v) {
+  reinterpret_cast<float*>(p)[idx] = tf32_rne(__double2float_rn(v));
+}
+template <> __device__ __forceinline__ void store_op<2>(void* p, long idx, double v) {
+  reinterpret_cast<__nv_bfloat16*>(p)[idx] = __double2bfloat16(v);
+}
+template <> __device__ __forceinline__ void store_op<3>(void* p, long idx, double v) {
+  reinterpret_cast<__half*>(p)[idx] = __double2half(v);
+}
+
+template <int OP, typename TD>
+__global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict__ N, const TD* __restrict__ D,
+                                                             void* Nq, long n, long ld, double alpha,
+                                                             double* partials, unsigned* counter, double* out3) {
+  __shared__ double s1[UPD_THREADS / 32], s2[UPD_THREADS / 32];
+  __shared__ bool is_last;
+  const double oma = 1.0 - alpha;
+  double dd = 0.0, nn = 0.0;
+  for (long i = blockIdx.x; i < n; i += gridDim.x) {
+    double* nr = N + i * ld;
+    const TD* dr = D + i * ld;
+    for (long j = threadIdx.x; j < n; j += UPD_THREADS) {
+      const double old = nr[j];
+      const double nv = __dadd_rn(__dmul_rn(oma, old), __dmul_rn(alpha, (double)dr[j]));
+      const double df = __dsub_rn(nv, old);
+      dd = __fma_rn(df, df, dd);
+      nn = __fma_rn(nv, nv, nn);
+      nr[j] = nv;
+      store_op<OP>(Nq, i * ld + j, nv);
+    }
+  }
+  dd = warp_sum_d(dd);
+  nn = warp_sum_d(nn);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) { s1[warp] = dd; s2[warp] = nn; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < UPD_THREADS / 32; ++w) { a += s1[w]; b += s2[w]; }
+    partials[2 * blockIdx.x] = a;
+    partials[2 * blockIdx.x + 1] = b;
+    __threadfence();
+    const unsigned done = atomicAdd(counter, 1u);
+    is_last = (done == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last && threadIdx.x == 0) {
+    __threadfence();
+    double a = 0.0, b = 0.0;
+    for (unsigned k = 0; k < gridDim.x; ++k) { a += __ldcg(partials + 2 * k); b += __ldcg(partials + 2 * k + 1); }
+    out3[0] = a;
+    out3[1] = b;
+    out3[2] = sqrt(a) / sqrt(b);
+    *counter = 0u;
+  }
+}
+
+template <int OP>
+__global__ void init_n_kernel(double* N, void* Nq, const double* X0, long n, long ld) {
+  const double u = 1.0 / (double)n;
+  for (long i = blockIdx.x; i < n; i += gridDim.x)
+    for (long j = threadIdx.x; j < n; j += blockDim.x) {
+      const double v = X0 ? X0[i * n + j] : u;
+      N[i * ld + j] = v;
+      store_op<OP>(Nq, i * ld + j, v);
+    }
+}
+
+__global__ void copy2d_kernel(double* dst, long ldd, const double* src, long lds, long rows, long cols) {
+  for (long i = blockIdx.x; i < rows; i += gridDim.x)
+    for (long j = threadIdx.x; j < cols; j += blockDim.x) dst[i * ldd + j] = src[i * lds + j];
+}
+
+}  // namespace
+
+cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long n, long ld, double alpha,
+                          double* partials, unsigned* counter, double* out3, cudaStream_t st, int num_sms) {
+  const int grid = (int)((n < (long)num_sms * 4) ? n : (long)num_sms * 4);
+#define UPD_CASE(OPV)                                                                                        \
+  if (d_f64) update_kernel<OPV, double><<<grid, UPD_THREADS, 0, st>>>(N, (const double*)D, Nq, n, ld, alpha, \
+                                                                    partials, counter, out3);                \
+  else update_kernel<OPV, float><<<grid, UPD_THREADS, 0, st>>>(N, (const float*)D, Nq, n, ld, alpha,         \
+                                                             partials, counter, out3);
+  switch (op) {
+    case 0: UPD_CASE(0) break;
+    case 1: UPD_CASE(1) break;
+    case 2: UPD_CASE(2) break;
+    case 3: UPD_CASE(3) break;
+    default: return cudaErrorInvalidValue;
+  }
+#undef UPD_CASE
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long n, long ld, cudaStream_t st) {
+  const int grid = (int)(n < 1024 ? n : 1024);
+  switch (op) {
+    case 0: init_n_kernel<0><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
+    case 1: init_n_kernel<1><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
+    case 2: init_n_kernel<2><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
+    case 3: init_n_kernel<3><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy2d_f64(double* dst, long ldd, const double* src, long lds, long rows, long cols,
+                              cudaStream_t st) {
+  const int grid = (int)(rows < 1024 ? rows : 1024);
+  copy2d_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(dst, ldd, src, lds, rows, cols);
+  return cudaGetLastError();
+}
+
+}  // namespace fram

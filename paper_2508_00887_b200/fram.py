@@ -1,0 +1,303 @@
+"""Thin ctypes binding of libfram.so (include/fram.h) — argument marshalling only.
+
+Every arithmetic step of FRAM runs in the library's CUDA kernels; this module only converts
+torch tensors / numpy arrays to pointers, builds the C structs and raises on error statuses.
+There is no CPU fallback: if libfram.so is missing or no sm_100 device is present, calls fail
+loudly.  Function names follow the C ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfram.so")
+
+FRAM_OK, FRAM_ERR_USAGE, FRAM_ERR_DATA, FRAM_NOT_CONVERGED, FRAM_ERR_CUDA, FRAM_ERR_NCCL, FRAM_ERR_OOM = range(7)
+STATUS_NAMES = ["OK", "ERR_USAGE", "ERR_DATA", "NOT_CONVERGED", "ERR_CUDA", "ERR_NCCL", "ERR_OOM"]
+PREC = {"fp64": 0, "tf32": 1, "bf16": 2, "fp16": 3}
+DT = {"f64": 0, "f32": 1, "bf16": 2}
+FLAG_TRACE, FLAG_CHECK_SYMMETRY, FLAG_NO_THETA_SCALE, FLAG_TIME_PHASES = 1, 2, 4, 8
+
+EXPORTED = ["fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_destroy",
+            "fram_last_error", "fram_get_unique_id", "fram_create_sharded", "fram_sdsn", "fram_gradient",
+            "fram_lap", "fram_abi_version", "fram_build_info"]
+
+
+class FramError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES[status] if 0 <= status < 7 else status}: {msg}")
+        self.status = status
+
+
+class _Schedule(C.Structure):
+    _fields_ = [("theta", C.c_double), ("alpha", C.c_double), ("gamma_th", C.c_double), ("delta_th", C.c_double),
+                ("max_outer", C.c_int32), ("sdsn_max", C.c_int32), ("sdsn_fixed", C.c_int32), ("flags", C.c_int32),
+                ("replay_passes", C.POINTER(C.c_int32)), ("replay_len", C.c_int32)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("outer_iters", C.c_int32), ("converged", C.c_int32), ("sdsn_capped_calls", C.c_int32),
+                ("_pad", C.c_int32), ("total_passes", C.c_int64), ("passes_per_iter", C.POINTER(C.c_int32)),
+                ("delta_trace", C.POINTER(C.c_double)), ("gamma_last", C.POINTER(C.c_double)),
+                ("ms_precond", C.c_double), ("ms_gemm", C.c_double), ("ms_sdsn", C.c_double),
+                ("ms_update", C.c_double), ("ms_lap", C.c_double), ("ms_total", C.c_double),
+                ("kernel_launches", C.c_int64)]
+
+
+@dataclass
+class Schedule:
+    """fram_schedule (include/fram.h); defaults = SURVEY §8(d) / P:374."""
+    theta: float = 10.0
+    alpha: float = 0.95
+    gamma_th: float = 1e-3
+    delta_th: float = 1e-4
+    max_outer: int = 100
+    sdsn_max: int = 1000
+    sdsn_fixed: int = 0
+    flags: int = FLAG_CHECK_SYMMETRY | FLAG_TRACE
+    replay: list | None = None
+
+    def to_c(self):
+        s = _Schedule(self.theta, self.alpha, self.gamma_th, self.delta_th, self.max_outer, self.sdsn_max,
+                      self.sdsn_fixed, self.flags, None, 0)
+        keep = None
+        if self.replay:
+            keep = (C.c_int32 * len(self.replay))(*[int(x) for x in self.replay])
+            s.replay_passes = C.cast(keep, C.POINTER(C.c_int32))
+            s.replay_len = len(self.replay)
+        return s, keep
+
+
+_lib_handle = None
+
+
+def lib():
+    """Load libfram.so (fails loudly if it has not been built)."""
+    global _lib_handle
+    if _lib_handle is not None:
+        return _lib_handle
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2508_00887_b200.build` "
+                           "(there is no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, i32, dbl = C.c_void_p, C.c_int64, C.c_int32, C.c_double
+    L.fram_create.argtypes = [i64, dbl, C.POINTER(_Schedule), C.c_int, C.POINTER(vp)]
+    L.fram_set_schedule.argtypes = [vp, C.POINTER(_Schedule)]
+    L.fram_solve.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, vp, C.POINTER(_Stats)]
+    L.fram_solve_batched.argtypes = [vp, i64, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, vp, vp, C.POINTER(_Stats)]
+    L.fram_destroy.argtypes = [vp]
+    L.fram_destroy.restype = None
+    L.fram_last_error.restype = C.c_char_p
+    L.fram_get_unique_id.argtypes = [C.c_char_p]
+    L.fram_create_sharded.argtypes = [i64, dbl, C.POINTER(_Schedule), C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(vp)]
+    L.fram_sdsn.argtypes = [vp, C.c_int, vp, vp, C.POINTER(i32), vp, vp]
+    L.fram_gradient.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, C.POINTER(dbl)]
+    L.fram_lap.argtypes = [vp, vp, vp, vp]
+    L.fram_build_info.restype = C.c_char_p
+    for f in ("fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_get_unique_id",
+              "fram_create_sharded", "fram_sdsn", "fram_gradient", "fram_lap"):
+        getattr(L, f).restype = C.c_int
+    _lib_handle = L
+    return L
+
+
+def _err(status):
+    return FramError(status, lib().fram_last_error().decode(errors="replace"))
+
+
+def _check(status, allow_nc=False):
+    if status == FRAM_OK or (allow_nc and status == FRAM_NOT_CONVERGED):
+        return status
+    raise _err(status)
+
+
+def _is_torch(x):
+    return type(x).__module__.startswith("torch")
+
+
+def _ptr(x):
+    if x is None:
+        return None
+    if _is_torch(x):
+        if not x.is_contiguous():
+            raise ValueError("tensor must be contiguous")
+        return C.c_void_p(x.data_ptr())
+    if isinstance(x, np.ndarray):
+        if not x.flags.c_contiguous:
+            raise ValueError("array must be C-contiguous")
+        return C.c_void_p(x.ctypes.data)
+    raise TypeError(f"unsupported buffer type {type(x)}")
+
+
+def _dt_of(x):
+    if _is_torch(x):
+        import torch
+        return {torch.float64: 0, torch.float32: 1, torch.bfloat16: 2}[x.dtype]
+    return {np.dtype(np.float64): 0, np.dtype(np.float32): 1}[x.dtype]
+
+
+def _stream(stream, *bufs):
+    if stream is not None:
+        return C.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+    for b in bufs:
+        if b is not None and _is_torch(b) and b.is_cuda:
+            import torch
+            return C.c_void_p(torch.cuda.current_stream(b.device).cuda_stream)
+    return None
+
+
+def _like(ref, shape, kind):
+    """Allocate an output on the same side (device/host) as `ref`."""
+    if _is_torch(ref):
+        import torch
+        dt = torch.float64 if kind == "f64" else torch.int32
+        return torch.empty(shape, dtype=dt, device=ref.device)
+    return np.empty(shape, dtype=np.float64 if kind == "f64" else np.int32)
+
+
+class Handle:
+    """Owns a fram_handle (fram_create / fram_destroy)."""
+
+    def __init__(self, ptr, n):
+        self.ptr = ptr
+        self.n = n
+
+    def __del__(self):
+        try:
+            if self.ptr:
+                lib().fram_destroy(self.ptr)
+        except Exception:
+            pass
+        self.ptr = None
+
+    @property
+    def _as_arg(self):
+        return self.ptr
+
+
+def fram_create(n, lam=1.0, schedule: Schedule | None = None, device=0) -> Handle:
+    s, keep = (schedule or Schedule()).to_c()
+    out = C.c_void_p()
+    _check(lib().fram_create(int(n), float(lam), C.byref(s), int(device), C.byref(out)))
+    del keep
+    return Handle(out, int(n))
+
+
+def fram_set_schedule(h: Handle, schedule: Schedule):
+    s, keep = schedule.to_c()
+    _check(lib().fram_set_schedule(h.ptr, C.byref(s)))
+    del keep
+
+
+def _stats_dict(st, nout, arrays):
+    d = dict(outer_iters=st.outer_iters, converged=bool(st.converged), sdsn_capped_calls=st.sdsn_capped_calls,
+             total_passes=int(st.total_passes), ms_precond=st.ms_precond, ms_gemm=st.ms_gemm,
+             ms_sdsn=st.ms_sdsn, ms_update=st.ms_update, ms_lap=st.ms_lap, ms_total=st.ms_total,
+             kernel_launches=int(st.kernel_launches))
+    if arrays is not None:
+        t = st.outer_iters
+        d["passes"] = [int(x) for x in arrays[0][:t]]
+        d["deltas"] = [float(x) for x in arrays[1][:t]]
+        d["gamma_last"] = [float(x) for x in arrays[2][:t]]
+    return d
+
+
+def fram_solve(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, X_out=None, perm_out=None,
+               max_outer=1000):
+    """Alg. 1 end to end.  Returns (status, stats, X_out, perm_out); raises FramError on errors."""
+    n = h.n
+    X_out = _like(A, (n, n), "f64") if X_out is None else X_out
+    perm_out = _like(A, (n,), "i32") if perm_out is None else perm_out
+    arrays = ((C.c_int32 * max_outer)(), (C.c_double * max_outer)(), (C.c_double * max_outer)())
+    st = _Stats()
+    st.passes_per_iter = C.cast(arrays[0], C.POINTER(C.c_int32))
+    st.delta_trace = C.cast(arrays[1], C.POINTER(C.c_double))
+    st.gamma_last = C.cast(arrays[2], C.POINTER(C.c_double))
+    status = lib().fram_solve(h.ptr, _dt_of(A), _ptr(A), _ptr(B), _ptr(K), _ptr(X0), PREC[precision],
+                              _stream(stream, A), _ptr(X_out), _ptr(perm_out), C.byref(st))
+    _check(status, allow_nc=True)
+    return status, _stats_dict(st, n, arrays), X_out, perm_out
+
+
+def fram_solve_batched(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, X_out=None,
+                       perm_out=None, status_out=None):
+    """`batch` independent solves (A, B, K: batch×n×n).  Returns (status, stats, X_out, perm_out, status_out)."""
+    n = h.n
+    batch = A.shape[0]
+    X_out = _like(A, (batch, n, n), "f64") if X_out is None else X_out
+    perm_out = _like(A, (batch, n), "i32") if perm_out is None else perm_out
+    status_out = np.zeros(batch, dtype=np.int32) if status_out is None else status_out
+    st = _Stats()
+    status = lib().fram_solve_batched(h.ptr, int(batch), _dt_of(A), _ptr(A), _ptr(B), _ptr(K), _ptr(X0),
+                                      PREC[precision], _stream(stream, A), _ptr(X_out), _ptr(perm_out),
+                                      _ptr(status_out), C.byref(st))
+    if status not in (FRAM_OK, FRAM_NOT_CONVERGED, FRAM_ERR_DATA):
+        raise _err(status)
+    return status, _stats_dict(st, n, None), X_out, perm_out, status_out
+
+
+def fram_sdsn(h: Handle, X, precision="fp32", D_out=None, stream=None, want_gammas=True, cap=None):
+    """One SDSN call (Alg. 2).  precision 'fp64' (X float64) or anything else (X float32).
+    Returns (D, passes, gammas)."""
+    p = 0 if precision == "fp64" else 2
+    if D_out is None:
+        if _is_torch(X):
+            import torch
+            D_out = torch.empty_like(X)
+        else:
+            D_out = np.empty_like(X)
+    passes = C.c_int32(0)
+    cap = cap or 200000
+    gh = (C.c_double * cap)() if want_gammas else None
+    _check(lib().fram_sdsn(h.ptr, p, _ptr(X), _ptr(D_out), C.byref(passes),
+                           C.cast(gh, C.c_void_p) if gh is not None else None, _stream(stream, X)))
+    k = passes.value
+    gam = [float(gh[i]) for i in range(k)] if gh is not None else None
+    return D_out, k, gam
+
+
+def fram_gradient(h: Handle, A, B, K, N, precision="bf16", stream=None, G_out=None):
+    """Preconditioning + G = A'·N·Ã' + λK'.  Returns (G, c)."""
+    n = h.n
+    if G_out is None:
+        if _is_torch(A):
+            import torch
+            G_out = torch.empty((n, n), dtype=torch.float64 if precision == "fp64" else torch.float32,
+                                device=A.device)
+        else:
+            G_out = np.empty((n, n), dtype=np.float64 if precision == "fp64" else np.float32)
+    c = C.c_double(0)
+    _check(lib().fram_gradient(h.ptr, _dt_of(A), _ptr(A), _ptr(B), _ptr(K), _ptr(N), PREC[precision],
+                               _stream(stream, A), _ptr(G_out), C.byref(c)))
+    return G_out, c.value
+
+
+def fram_lap(h: Handle, N, perm_out=None, stream=None):
+    """Deterministic Hungarian (R17) on FP64 N.  Returns perm (int32)."""
+    perm_out = _like(N, (h.n,), "i32") if perm_out is None else perm_out
+    _check(lib().fram_lap(h.ptr, _ptr(N), _ptr(perm_out), _stream(stream, N)))
+    return perm_out
+
+
+def fram_get_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().fram_get_unique_id(buf))
+    return buf.raw
+
+
+def fram_create_sharded(n, lam, schedule: Schedule | None, uid: bytes, rank, world, device=0) -> Handle:
+    s, keep = (schedule or Schedule()).to_c()
+    out = C.c_void_p()
+    _check(lib().fram_create_sharded(int(n), float(lam), C.byref(s), uid, int(rank), int(world), int(device),
+                                     C.byref(out)))
+    del keep
+    return Handle(out, int(n))
+
+
+def fram_build_info() -> str:
+    return lib().fram_build_info().decode()

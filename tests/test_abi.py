@@ -1,0 +1,68 @@
+"""CPU-side checks of the C-ABI boundary: the library loads and exports every declared symbol;
+argument validation that needs no GPU."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+import paper_2508_00887_b200 as fb
+from paper_2508_00887_b200 import fram as F
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "fram.h")).read()
+    return sorted(set(re.findall(r"FRAM_API\s+[\w\s\*]+?\b(fram_\w+)\s*\(", src)))
+
+
+def test_header_declares_abi():
+    names = _declared()
+    for required in ("fram_create", "fram_solve", "fram_solve_batched", "fram_destroy", "fram_sdsn",
+                     "fram_gradient", "fram_lap", "fram_get_unique_id", "fram_create_sharded"):
+        assert required in names
+
+
+def test_library_exports_every_symbol():
+    L = fb.lib()
+    for name in _declared():
+        assert hasattr(L, name), name
+    assert sorted(F.EXPORTED) == _declared()
+    assert L.fram_abi_version() == 1
+    assert "sm_100a" in fb.fram_build_info()
+
+
+def test_create_validation():
+    with pytest.raises(fb.FramError) as e:
+        fb.fram_create(0)
+    assert e.value.status == fb.FRAM_ERR_USAGE
+    with pytest.raises(fb.FramError):
+        fb.fram_create(10, lam=-1.0)
+    with pytest.raises(fb.FramError):
+        fb.fram_create(10, schedule=fb.Schedule(theta=0.0))
+    with pytest.raises(fb.FramError):
+        fb.fram_create(10, schedule=fb.Schedule(alpha=1.5))
+    with pytest.raises(fb.FramError):
+        fb.fram_create(10, schedule=fb.Schedule(replay=[3, 0]))
+    h = fb.fram_create(10, schedule=fb.Schedule(replay=[3, 4]))
+    fb.fram_set_schedule(h, fb.Schedule(theta=2.0))
+    del h
+
+
+def test_sharded_create_validation():
+    with pytest.raises(fb.FramError) as e:
+        fb.fram_create_sharded(10, 1.0, None, b"\0" * 128, rank=0, world=3)
+    assert e.value.status == fb.FRAM_ERR_USAGE
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    import numpy as np
+    h = fb.fram_create(8)
+    A = np.eye(8)
+    with pytest.raises(fb.FramError) as e:
+        fb.fram_solve(h, A, A)
+    assert e.value.status == fb.FRAM_ERR_CUDA
