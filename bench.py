@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py — FRAM iterations/s and time-to-solution at n=4096 (BASELINE.json `metric`, config C4).
+
+One *step* = one complete fram_solve (Alg. 1: preconditioning, the outer loop of
+tcgen05 gradient GEMMs + SDSN passes + FP64 update/δ, and the final GPU Hungarian) on the C4
+workload: Barabási–Albert n=4096 (m=5), Ã = P·A·Pᵀ with 5% edge rewiring, X0 = 11ᵀ/n,
+bf16-GEMM / fp32-SDSN, θ=10, α=0.95, λ=1, γ_th=1e-3, δ_th=1e-4, sdsn_max=1000, max_outer=100.
+`value` = outer iterations of all ranks ÷ max-over-ranks device time of the K timed steps.
+
+Multi-GPU (--gpus N, torchrun): C4 does not shard: each rank solves an independent
+replica (seed = rank), no data-path collective ("scaling": "weak").
+
+--impl reference: the FP64 CPU oracle (oracle/) as it stands, on a bounded sample of the same
+workload (one gradient + a few SDSN passes + one update per step, extrapolated to iterations/s).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FRAM iters/s & time-to-solution at n=4096; GEMM TC util %, SDSN HBM GB/s"
+UNIT = "outer iterations/s"
+WORKLOAD = "C4: BA(m=5) n=4096, 5% rewiring, X0=11^T/n, bf16-GEMM/fp32-SDSN, theta=10"
+SCHEDULE = dict(theta=10.0, alpha=0.95, lam=1.0, gamma_th=1e-3, delta_th=1e-4, sdsn_max=1000, max_outer=100)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=3)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "fp16", "fp64"])
+    p.add_argument("--n", type=int, default=4096, help="dev override (the metric is quoted at 4096)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), \
+            "MEASURED_PEAKS.json"
+    except Exception:
+        return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = max(smax, float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sm if s > 0.5 * smax] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info() if i.get("user_api") == "blas"] or [1])
+    except Exception:
+        return 1
+
+
+def oracle_sample(inst, passes_per_iter, budget_s=12.0):
+    """Time the FP64 oracle (as it stands) on a bounded sample of one outer iteration of the workload:
+    precondition, one gradient (two BLAS GEMMs), a few SDSN passes, one update; extrapolate one outer
+    iteration to `passes_per_iter` SDSN passes.  Returns (iters_per_s, seconds_used, description)."""
+    import numpy as np
+    import oracle
+
+    t0 = time.perf_counter()
+    Ap, Bp, Kp, c = oracle.precondition(inst.A, inst.B, inst.K)
+    n = inst.n
+    N = np.full((n, n), 1.0 / n)
+    tg = time.perf_counter()
+    G = oracle.gradient(Ap, N, Bp, Kp, 1.0)
+    t_grad = time.perf_counter() - tg
+    ts = time.perf_counter()
+    oracle.sdsn(G, inst.theta, sdsn_fixed=2, check_nonneg=False)
+    t2 = (time.perf_counter() - ts) / 2
+    k = int(max(2, min(200, (budget_s - (time.perf_counter() - t0)) / max(t2, 1e-6))))
+    ts = time.perf_counter()
+    D, _ = oracle.sdsn(G, inst.theta, sdsn_fixed=k, check_nonneg=False)
+    t_pass = (time.perf_counter() - ts) / k
+    tu = time.perf_counter()
+    N_new = (1.0 - 0.95) * N + 0.95 * D
+    float(np.linalg.norm(N_new - N) / np.linalg.norm(N_new))
+    t_upd = time.perf_counter() - tu
+    it = t_grad + passes_per_iter * t_pass + t_upd
+    desc = (f"FP64 NumPy oracle on the {inst.name} n={n} input: 1 gradient (2 BLAS GEMMs) {t_grad:.2f}s + {k} "
+            f"SDSN passes at {t_pass * 1e3:.1f} ms/pass (single-threaded NumPy) + 1 update {t_upd:.2f}s, timed; "
+            f"one outer iteration extrapolated to {passes_per_iter:.0f} passes/iteration")
+    return 1.0 / it, time.perf_counter() - t0, desc, t_pass, t_grad
+
+
+def run_reference(args):
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    from synth import config_c4
+    inst = config_c4(0, n=args.n)
+    ppi = float(SCHEDULE["sdsn_max"])    # at C4 the 1000-pass cap binds on every call after t=1 (R3, [M16])
+    for _ in range(args.warmup):
+        oracle_sample(inst, ppi, budget_s=4.0)
+    vals, secs = [], []
+    desc = ""
+    for _ in range(args.steps):
+        v, s, desc, _, _ = oracle_sample(inst, ppi, budget_s=8.0)
+        vals.append(v)
+        secs.append(s)
+    value = statistics.median(vals)
+    cores = blas_threads()
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded C4 generator; SNAP Facebook-ego stand-in)",
+            "config": {"workload": WORKLOAD, "n": args.n, "schedule": SCHEDULE, "seed": 0},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_00887_b200 as fb
+    from synth import config_c4
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    inst = config_c4(seed=rank, n=args.n)
+    n = inst.n
+    A = torch.tensor(inst.A, dtype=torch.float32, device=dev)
+    B = torch.tensor(inst.B, dtype=torch.float32, device=dev)
+    flags = fb.FLAG_TRACE | fb.FLAG_CHECK_SYMMETRY | fb.FLAG_TIME_PHASES
+    sch = fb.Schedule(theta=inst.theta, alpha=SCHEDULE["alpha"], gamma_th=SCHEDULE["gamma_th"],
+                      delta_th=SCHEDULE["delta_th"], max_outer=SCHEDULE["max_outer"],
+                      sdsn_max=SCHEDULE["sdsn_max"], flags=flags)
+    h = fb.fram_create(n, lam=SCHEDULE["lam"], schedule=sch, device=local)
+    X = torch.empty((n, n), dtype=torch.float64, device=dev)
+    perm = torch.empty((n,), dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        fb.fram_solve(h, A, B, precision=args.precision, X_out=X, perm_out=perm)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)     # 256 MiB > 126 MB L2
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    stats = []
+    for k in range(args.steps):
+        flush.fill_(float(k))                                         # L2 flush, outside the events
+        ev[k][0].record()
+        st, s, _, _ = fb.fram_solve(h, A, B, precision=args.precision, X_out=X, perm_out=perm)
+        ev[k][1].record()
+        stats.append(s)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    iters = sum(s["outer_iters"] for s in stats)
+    passes = sum(s["total_passes"] for s in stats)
+    launches = sum(s["kernel_launches"] for s in stats)
+    ms_sdsn = sum(s["ms_sdsn"] for s in stats)
+    ms_gemm = sum(s["ms_gemm"] for s in stats)
+    ms_lap = sum(s["ms_lap"] for s in stats)
+    acc = float((perm.cpu().numpy() == inst.perm_true).mean())
+    if world > 1:
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms_all = float(t.item())
+        it = torch.tensor([iters], dtype=torch.float64, device=dev)
+        dist.all_reduce(it, op=dist.ReduceOp.SUM)
+        iters_all = float(it.item())
+    else:
+        tot_ms_all, iters_all = tot_ms, float(iters)
+    value = iters_all / (tot_ms_all / 1e3)
+
+    # ---- e2e: same solve through the C ABI with pinned HOST buffers (H2D/D2H inside the region)
+    e2e = None
+    if not args.no_e2e:
+        Ah = A.cpu().pin_memory()
+        Bh = B.cpu().pin_memory()
+        Xh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        ph = torch.empty((n,), dtype=torch.int32).pin_memory()
+        fb.fram_solve(h, Ah, Bh, precision=args.precision, X_out=Xh, perm_out=ph,
+                      stream=torch.cuda.current_stream(dev))
+        barrier()
+        torch.cuda.synchronize()
+        e_ms, e_it = 0.0, 0
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _, s, _, _ = fb.fram_solve(h, Ah, Bh, precision=args.precision, X_out=Xh, perm_out=ph,
+                                       stream=torch.cuda.current_stream(dev))
+            b.record()
+            b.synchronize()
+            e_ms += a.elapsed_time(b)
+            e_it += s["outer_iters"]
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+            it = torch.tensor([e_it], dtype=torch.float64, device=dev)
+            dist.all_reduce(it, op=dist.ReduceOp.SUM)
+            e_it = float(it.item())
+        e2e = {"value": e_it / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Ah.nbytes + Bh.nbytes),
+               "d2h_bytes_per_step": int(Xh.nbytes + ph.nbytes)}
+
+    hbm, bf16, bf16s, psrc = peaks()
+    sdsn_launches = iters                                     # one persistent SDSN launch per outer iteration
+    bytes_per_launch = 8.0 * n * n * passes / sdsn_launches   # algorithmic: FP32 Y read + write per pass
+    avg_launch_s = ms_sdsn / 1e3 / sdsn_launches
+    achieved = bytes_per_launch / avg_launch_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "sdsn_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if int(tj.get("n", 0)) == n:
+                traffic = float(tj["dram_bytes_per_pass"]) * passes / sdsn_launches
+        except Exception:
+            traffic = None
+    gemm_tflops = 4.0 * n ** 3 * iters / (ms_gemm / 1e3) / 1e12 if ms_gemm > 0 else None
+
+    line = None
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms_all / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "bf16-gemm/f32-sdsn/f64-update"
+                if args.precision != "fp64" else "f64",
+                "data": "synthetic (seeded C4 generator; SNAP Facebook-ego stand-in)",
+                "config": {"workload": WORKLOAD, "n": n, "precision": args.precision, "schedule": SCHEDULE,
+                           "seed": "rank", "replicas": world, "l2": "flushed between steps (256 MiB write)",
+                           "parallelism": f"{world} independent replicas (C4 does not shard, SURVEY 8(e))"},
+                "time_to_solution_ms": statistics.median(step_ms),
+                "outer_iters_per_solve": iters / args.steps, "mean_passes_per_iter": passes / iters,
+                "accuracy": acc,
+                "roofline": {"kernel": "sdsn_kernel<float,2> (K4, one persistent launch per SDSN call)",
+                             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                             "frac": achieved / hbm, "traffic": traffic, "peak_source": psrc,
+                             "algorithmic_bytes_per_launch": bytes_per_launch,
+                             "passes_per_launch": passes / sdsn_launches,
+                             "share_of_step": ms_sdsn / tot_ms},
+                "gemm": {"tflops": gemm_tflops, "peak_bf16": bf16s, "frac_of_sustained": (gemm_tflops or 0) / bf16s,
+                         "ms_per_step": ms_gemm / args.steps},
+                "lap_ms_per_step": ms_lap / args.steps,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+    if world > 1:
+        dist.barrier()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        mean_ppi = passes / iters
+        v, secs, desc, _, _ = oracle_sample(inst, mean_ppi, budget_s=15.0)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "oracle", "sample": desc}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

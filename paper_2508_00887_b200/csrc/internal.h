@@ -19,6 +19,7 @@ struct SdsnParams {
   int* passes_out;     // [1]
   double* gamma_hist;  // [sdsn_max] nullable: γ_j of every pass input
   double* sdsn_out;    // [4]: [0] γ of the last pass input, [1] max X, [2] S of last input
+  int debug;           // dev-only timing knobs (FRAM_SDSN_DEBUG): 1 skip sweeps, 2 skip barriers/reductions
 };
 // f64: T=double; else T=float.  Returns the grid used via *grid_out.
 cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_sms, int* grid_out);

@@ -8,14 +8,18 @@
 //   and, fused into the same sweep, the row sums, column partials and mass of Y_{j+1}.
 // Stop after pass j iff (j ≥ 1 ∧ γ_j ≤ γ_th) ∨ j+1 = sdsn_max (R5, R16) — known BEFORE the pass.
 //
-// Data layout: Y row-major n×ld in HBM (T = float in mixed modes, double in FP64 mode); CTA b
-// owns rows [b·n/G, (b+1)·n/G); thread t owns 16-byte column vectors q = t + k·THREADS.
-//   row sums  : per-thread partials → warp shuffle → fixed-order cross-warp sum (FP64) — local;
-//   col sums  : per-thread register partials over the CTA's rows → colpart[b][:] →
-//               grid barrier → CTA b reduces column slice b over all CTAs in a fixed order
-//               (deterministic, no float atomics: S:375) → grid barrier.
-//   S         : Σ per-CTA row-sum partials, summed identically by every CTA (FP64).
-// Bytes per pass: 8n² (FP32) / 16n² (FP64) of Y + O(G·n) partials.
+// Data layout and work split: Y row-major n×ld (T = float in mixed modes, double in FP64 mode).
+// CTA b owns rows [b·n/G, (b+1)·n/G).  Its 16 warps form CG column groups × RG row groups
+// (CG·RG = 16); a warp streams every row of its row group over its column slice, with a register
+// ring keeping PD rows of 16-byte loads in flight (no CTA barrier inside the sweep):
+//   row sums : warp shuffle per row → s_rowpart[row][cg] → fixed-order sum over cg (FP64);
+//   col sums : per-lane register partials over the warp's rows → (RG>1: fixed-order smem combine)
+//              → colpart[b][:] → grid barrier → CTA b reduces column slice b over all CTAs in a
+//              fixed order (deterministic, no float atomics: S:375) → grid barrier;
+//   S        : Σ per-CTA row-sum partials, summed identically by every CTA (FP64).
+// Algorithmic bytes per pass: 8n² (FP32) / 16n² (FP64) of Y, + O(G·n) of partials.
+#include <stdlib.h>
+#include <type_traits>
 #include "common.cuh"
 #include "internal.h"
 
@@ -41,45 +45,36 @@ __device__ __forceinline__ double tmax0(double x) { return fmax(0.0, x); }
 __device__ __forceinline__ float warp_sum_t(float v) { return warp_sum_f(v); }
 __device__ __forceinline__ double warp_sum_t(double v) { return warp_sum_d(v); }
 
-// Fixed-order block reduction of RB per-thread row partials → s_r[row0 .. row0+cnt) (FP64).
-template <typename T, int RB>
-__device__ __forceinline__ void block_rows_reduce(T (&acc)[RB], double (*s_part)[kSdsnWarps][RB],
-                                                  int buf, double* s_r, int row0, int cnt) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int rr = 0; rr < RB; ++rr) {
-    T v = warp_sum_t(acc[rr]);
-    if (lane == 0) s_part[buf][warp][rr] = (double)v;
-  }
-  __syncthreads();
-  if (threadIdx.x < cnt) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < kSdsnWarps; ++w) s += s_part[buf][w][threadIdx.x];
-    s_r[row0 + threadIdx.x] = s;
-  }
-}
+enum { SWEEP_SCALE = 0, SWEEP_PASS = 1 };
 
-template <typename T, int NV>
-__global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
+template <typename T, int VPL>
+__global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int CG) {
   using VT = typename VecT<T>::t;
   constexpr int W = VecT<T>::W;
-  constexpr int RB = (8 / NV) > 0 ? (8 / NV) : 1;           // rows per chunk: 8 vectors in flight
+  constexpr int PD = VPL >= 8 ? 1 : 16 / VPL;                // rows in flight per warp
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const long rows_max = (P.n + gridDim.x - 1) / gridDim.x + 1;
+  double* s_rowpart = reinterpret_cast<double*>(dsm);       // [rows_max][CG]
+  T* s_colstage = reinterpret_cast<T*>(dsm + ((sizeof(double) * rows_max * CG + 15) & ~15ul));   // [RG][ld]
   __shared__ double s_r[kSdsnMaxRows];
   __shared__ T s_a[kSdsnMaxRows];
-  __shared__ double s_part[2][kSdsnWarps][RB];
   __shared__ double s_red[kSdsnWarps][32];
   __shared__ double s_scal[2];
 
   const unsigned G = gridDim.x;
   const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int RG = kSdsnWarps / CG;
+  const int cg = warp % CG, rg = warp / CG;
   const long n = P.n, ld = P.ld;
   const long r0 = (long)b * n / G, r1 = (long)(b + 1) * n / G;
   const int R = (int)(r1 - r0);
   const long nvec = (n + W - 1) / W;
+  const int nrw = (R > rg) ? (R - rg + RG - 1) / RG : 0;     // rows handled by this warp
   T* Y = reinterpret_cast<T*>(P.Y);
   T* colpart = reinterpret_cast<T*>(P.colpart);
-  const double dn = (double)n, nn = dn * dn, inv_n = 1.0 / dn;
+  const double dn = (double)n, nn = dn * dn;
+  // vector index of slot k for this lane: q = (cg·VPL + k)·32 + lane
+  auto qidx = [&](int k) -> long { return ((long)cg * VPL + k) * 32 + lane; };
 
   // ---------------- column-slice reduction + S (after barrier 1) ----------------
   auto reduce_columns_and_S = [&]() {
@@ -106,8 +101,117 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
       if (lane == 0) s_scal[0] = s;
     }
   };
-  // per-CTA Σ of own row sums (fixed order) → Spart[b]
-  auto publish_rows = [&]() {
+
+  // ---------------- one sweep over the CTA's rows ----------------
+  // MODE SCALE: y ← fl(s·y) (written only if P.scale); MODE PASS: y ← max(0, (y + a_i) + b_j).
+  // Both accumulate the row sums (s_r) and column partials (colpart[b]) of the new values.
+  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W]) {
+    constexpr int mode = decltype(mode_c)::value;
+    T colacc[VPL][W];
+#pragma unroll
+    for (int k = 0; k < VPL; ++k)
+#pragma unroll
+      for (int w = 0; w < W; ++w) colacc[k][w] = (T)0;
+    // per-slot constants (32-bit indexing: n·ld < 2^31 for every supported n)
+    const int ldv = (int)(ld / W);
+    VT* Yc = reinterpret_cast<VT*>(Y) + (long)r0 * ldv;        // this CTA's first row
+    int qv[VPL], kind[VPL];                                   // kind: 0 skip, 1 full vector, 2 tail
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) {
+      qv[k] = (int)qidx(k);
+      kind[k] = qv[k] >= (int)nvec ? 0 : ((qv[k] + 1) * W <= (int)n ? 1 : 2);
+    }
+    VT buf[PD][VPL];
+    auto load_row = [&](int s, int rr) {
+      const VT* row = Yc + (rg + rr * RG) * ldv;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+        if (kind[k]) buf[s][k] = __ldcg(row + qv[k]);
+    };
+    bool full = true;                                          // every slot a full vector?
+#pragma unroll
+    for (int k = 0; k < VPL; ++k) full = full && (kind[k] == 1);
+    full = __all_sync(0xffffffffu, full);
+#pragma unroll
+    for (int s = 0; s < PD; ++s)
+      if (s < nrw) load_row(s, s);
+    auto run = [&](auto full_c) {
+      constexpr bool FULL = decltype(full_c)::value;
+      for (int base = 0; base < nrw; base += PD) {
+        T rs[PD];
+#pragma unroll
+        for (int s = 0; s < PD; ++s) {
+          rs[s] = (T)0;
+          const int rr = base + s;
+          if (rr < nrw) {
+            const int il = rg + rr * RG;                     // local row index
+            VT* row = Yc + il * ldv;
+            const T a = (mode == SWEEP_PASS) ? s_a[il] : (T)0;
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) {
+              if (FULL || kind[k]) {
+                T e[W];
+                vget<T>(buf[s][k], e);
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                  T y;
+                  if constexpr (mode == SWEEP_PASS) y = tmax0((e[w] + a) + bv[k][w]);   // P2(P1(Y))
+                  else y = P.scale ? (T)(sc * (double)e[w]) : e[w];
+                  if (!FULL && kind[k] == 2 && qv[k] * W + w >= (int)n) y = (T)0;     // ragged tail
+                  e[w] = y;
+                  rs[s] += y;
+                  colacc[k][w] += y;
+                }
+                if (mode == SWEEP_PASS || P.scale) __stcg(row + qv[k], vmake<T>(e));
+              }
+            }
+            if (rr + PD < nrw) load_row(s, rr + PD);
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < PD; ++s) rs[s] = warp_sum_t(rs[s]);      // converged: PD chains interleave
+        if (lane == 0) {
+#pragma unroll
+          for (int s = 0; s < PD; ++s)
+            if (base + s < nrw) s_rowpart[(rg + (base + s) * RG) * CG + cg] = (double)rs[s];
+        }
+      }
+    };
+    if (full) run(std::true_type{});
+    else run(std::false_type{});
+    // column partials of this CTA → colpart[b]
+    if (RG == 1) {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const long q = qidx(k);
+        if (q < nvec) reinterpret_cast<VT*>(colpart + (long)b * ld)[q] = vmake<T>(colacc[k]);
+      }
+      __syncthreads();
+    } else {
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        const long q = qidx(k);
+        if (q < nvec) reinterpret_cast<VT*>(s_colstage + (long)rg * ld)[q] = vmake<T>(colacc[k]);
+      }
+      __syncthreads();
+      for (long q = tid; q < nvec; q += kSdsnThreads) {
+        T acc[W];
+        vget<T>(reinterpret_cast<const VT*>(s_colstage)[q], acc);
+        for (int g = 1; g < RG; ++g) {
+          T e[W];
+          vget<T>(reinterpret_cast<const VT*>(s_colstage + (long)g * ld)[q], e);
+#pragma unroll
+          for (int w = 0; w < W; ++w) acc[w] += e[w];
+        }
+        reinterpret_cast<VT*>(colpart + (long)b * ld)[q] = vmake<T>(acc);
+      }
+    }
+    // row sums (fixed order over column groups) and the CTA's mass partial
+    for (int i = tid; i < R; i += kSdsnThreads) {
+      double s = 0.0;
+      for (int g = 0; g < CG; ++g) s += s_rowpart[i * CG + g];
+      s_r[i] = s;
+    }
     __syncthreads();
     if (warp == 0) {
       double s = 0.0;
@@ -121,14 +225,14 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
   double sc = 1.0;
   if (P.scale) {
     double m = 0.0;
-    for (int i = 0; i < R; ++i) {
-      const VT* row = reinterpret_cast<const VT*>(Y + (r0 + i) * ld);
+    for (int rr = 0; rr < nrw; ++rr) {
+      const VT* row = reinterpret_cast<const VT*>(Y + (r0 + rg + (long)rr * RG) * ld);
 #pragma unroll
-      for (int k = 0; k < NV; ++k) {
-        const long q = tid + (long)k * kSdsnThreads;
+      for (int k = 0; k < VPL; ++k) {
+        const long q = qidx(k);
         if (q < nvec) {
           T e[W];
-          vget<T>(ldcg(row + q), e);
+          vget<T>(__ldcg(row + q), e);
 #pragma unroll
           for (int w = 0; w < W; ++w)
             if (q * W + w < n) m = fmax(m, (double)e[w]);
@@ -158,7 +262,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
         for (long q = tid; q < ld / W; q += kSdsnThreads) {
           T e[W];
 #pragma unroll
-          for (int w = 0; w < W; ++w) e[w] = (q * W + w < n) ? (T)inv_n : (T)0;
+          for (int w = 0; w < W; ++w) e[w] = (q * W + w < n) ? (T)(1.0 / dn) : (T)0;
           row[q] = vmake<T>(e);
         }
       }
@@ -173,49 +277,14 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
   }
 
   // ---------------- phase S: Y0 = s·X (in place) and its sums ----------------
-  T colacc[NV][W];
-#pragma unroll
-  for (int k = 0; k < NV; ++k)
-#pragma unroll
-    for (int w = 0; w < W; ++w) colacc[k][w] = (T)0;
   {
-    int buf = 0;
-    for (int i0 = 0; i0 < R; i0 += RB, buf ^= 1) {
-      T racc[RB];
+    T bz[VPL][W];
 #pragma unroll
-      for (int rr = 0; rr < RB; ++rr) {
-        racc[rr] = (T)0;
-        const int i = i0 + rr;
-        if (i < R) {
-          VT* row = reinterpret_cast<VT*>(Y + (r0 + i) * ld);
+    for (int k = 0; k < VPL; ++k)
 #pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            const long q = tid + (long)k * kSdsnThreads;
-            if (q < nvec) {
-              T e[W];
-              vget<T>(row[q], e);
-#pragma unroll
-              for (int w = 0; w < W; ++w) {
-                T y = P.scale ? (T)(sc * (double)e[w]) : e[w];
-                y = (q * W + w < n) ? y : (T)0;
-                e[w] = y;
-                racc[rr] += y;
-                colacc[k][w] += y;
-              }
-              if (P.scale) row[q] = vmake<T>(e);
-            }
-          }
-        }
-      }
-      block_rows_reduce<T, RB>(racc, s_part, buf, s_r, i0, min(RB, R - i0));
-    }
+      for (int w = 0; w < W; ++w) bz[k][w] = (T)0;
+    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz);
   }
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const long q = tid + (long)k * kSdsnThreads;
-    if (q < nvec) reinterpret_cast<VT*>(colpart + (long)b * ld)[q] = vmake<T>(colacc[k]);
-  }
-  publish_rows();
   grid_barrier(P.bar, G);
   reduce_columns_and_S();
   grid_barrier(P.bar, G);
@@ -231,68 +300,18 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
                                        : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
     const double abase = 1.0 / dn + S / nn;
     for (int i = tid; i < R; i += kSdsnThreads) s_a[i] = (T)(abase - s_r[i] / dn);
-    __syncthreads();
-    T bv[NV][W];                                                       // b for owned columns
+    T bv[VPL][W];                                                      // b for this lane's columns
 #pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const long q = tid + (long)k * kSdsnThreads;
+    for (int k = 0; k < VPL; ++k) {
+      const long q = qidx(k);
 #pragma unroll
       for (int w = 0; w < W; ++w)
         bv[k][w] = (q * W + w < n) ? (T)(-ldcg(P.cvec + q * W + w) / dn) : (T)0;
-#pragma unroll
-      for (int w = 0; w < W; ++w) colacc[k][w] = (T)0;
     }
-    int buf = 0;
-    for (int i0 = 0; i0 < R; i0 += RB, buf ^= 1) {
-      VT v[RB][NV];
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr) {
-        const int i = i0 + rr;
-        if (i < R) {
-          const VT* row = reinterpret_cast<const VT*>(Y + (r0 + i) * ld);
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            const long q = tid + (long)k * kSdsnThreads;
-            if (q < nvec) v[rr][k] = __ldcg(row + q);
-          }
-        }
-      }
-      T racc[RB];
-#pragma unroll
-      for (int rr = 0; rr < RB; ++rr) {
-        racc[rr] = (T)0;
-        const int i = i0 + rr;
-        if (i < R) {
-          const T a = s_a[i];
-          VT* row = reinterpret_cast<VT*>(Y + (r0 + i) * ld);
-#pragma unroll
-          for (int k = 0; k < NV; ++k) {
-            const long q = tid + (long)k * kSdsnThreads;
-            if (q < nvec) {
-              T e[W];
-              vget<T>(v[rr][k], e);
-#pragma unroll
-              for (int w = 0; w < W; ++w) {
-                T y = tmax0((e[w] + a) + bv[k][w]);                    // P2(P1(Y)) elementwise
-                y = (q * W + w < n) ? y : (T)0;
-                e[w] = y;
-                racc[rr] += y;
-                colacc[k][w] += y;
-              }
-              __stcg(row + q, vmake<T>(e));
-            }
-          }
-        }
-      }
-      block_rows_reduce<T, RB>(racc, s_part, buf, s_r, i0, min(RB, R - i0));
-    }
+    __syncthreads();
+    if (!(P.debug & 1)) sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv);
     if (last) break;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const long q = tid + (long)k * kSdsnThreads;
-      if (q < nvec) reinterpret_cast<VT*>(colpart + (long)b * ld)[q] = vmake<T>(colacc[k]);
-    }
-    publish_rows();
+    if (P.debug & 2) { __syncthreads(); continue; }
     grid_barrier(P.bar, G);
     reduce_columns_and_S();
     grid_barrier(P.bar, G);
@@ -304,18 +323,26 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P) {
   }
 }
 
-static int nv_for(long n, bool f64) {
+// VPL (16-byte vectors per lane per row slice) and CG (column groups, CG·RG = 16 warps).
+static bool plan(long n, bool f64, int* vpl, int* cg) {
   const int W = f64 ? 2 : 4;
   const long nvec = (n + W - 1) / W;
-  const long per = (nvec + kSdsnThreads - 1) / kSdsnThreads;
-  if (per <= 1) return 1;
-  if (per <= 2) return 2;
-  if (per <= 4) return 4;
-  if (per <= 8) return 8;
-  return 0;
+  int v = 1;
+  while (v <= 8 && (nvec + 32L * v * kSdsnWarps - 1) / (32L * v * kSdsnWarps) > 1) v *= 2;
+  if (v > 8) return false;
+  const long groups = (nvec + 32L * v - 1) / (32L * v);      // warps needed to cover a row
+  int c = 1;
+  while (c < groups) c *= 2;
+  if (c > kSdsnWarps) return false;
+  *vpl = v;
+  *cg = c;
+  return true;
 }
 
-bool sdsn_supported(long n, bool f64) { return n >= 1 && nv_for(n, f64) > 0; }
+bool sdsn_supported(long n, bool f64) {
+  int v, c;
+  return n >= 1 && plan(n, f64, &v, &c);
+}
 
 int sdsn_grid_for(long n, int num_sms) {
   long g = n / 16;
@@ -325,34 +352,41 @@ int sdsn_grid_for(long n, int num_sms) {
   return (int)g;
 }
 
-template <typename T, int NV>
-static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid) {
-  auto fn = sdsn_kernel<T, NV>;
+template <typename T, int VPL>
+static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int cg) {
+  auto fn = sdsn_kernel<T, VPL>;
+  const int RG = kSdsnWarps / cg;
+  const long rows_max = (p.n + grid - 1) / grid + 1;
+  const size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0);
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+  if (e != cudaSuccess) return e;
   SdsnParams pp = p;
-  void* args[] = {&pp};
-  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kSdsnThreads), args, 0, st);
+  if (const char* dbg = getenv("FRAM_SDSN_DEBUG")) pp.debug = atoi(dbg);
+  int cgv = cg;
+  void* args[] = {&pp, &cgv};
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kSdsnThreads), args, dsm, st);
 }
 
 cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_sms, int* grid_out) {
-  const int nv = nv_for(p.n, f64);
-  if (nv == 0) return cudaErrorInvalidValue;
+  int vpl, cg;
+  if (!plan(p.n, f64, &vpl, &cg)) return cudaErrorInvalidValue;
   const int grid = sdsn_grid_for(p.n, num_sms);
   if (grid_out) *grid_out = grid;
   cudaError_t e = cudaMemsetAsync(p.bar, 0, 2 * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   if (f64) {
-    switch (nv) {
-      case 1: return launch_t<double, 1>(p, st, grid);
-      case 2: return launch_t<double, 2>(p, st, grid);
-      case 4: return launch_t<double, 4>(p, st, grid);
-      default: return launch_t<double, 8>(p, st, grid);
+    switch (vpl) {
+      case 1: return launch_t<double, 1>(p, st, grid, cg);
+      case 2: return launch_t<double, 2>(p, st, grid, cg);
+      case 4: return launch_t<double, 4>(p, st, grid, cg);
+      default: return launch_t<double, 8>(p, st, grid, cg);
     }
   }
-  switch (nv) {
-    case 1: return launch_t<float, 1>(p, st, grid);
-    case 2: return launch_t<float, 2>(p, st, grid);
-    case 4: return launch_t<float, 4>(p, st, grid);
-    default: return launch_t<float, 8>(p, st, grid);
+  switch (vpl) {
+    case 1: return launch_t<float, 1>(p, st, grid, cg);
+    case 2: return launch_t<float, 2>(p, st, grid, cg);
+    case 4: return launch_t<float, 4>(p, st, grid, cg);
+    default: return launch_t<float, 8>(p, st, grid, cg);
   }
 }
 
