@@ -4,6 +4,8 @@
 // (to read δ and the SDSN pass count); the SDSN pass loop itself is device-resident.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -57,6 +59,7 @@ struct fram_ctx {
   long ld = 0;
   // workspace
   DevBuf Aq, BqT, Kq, N, Nq, UT, Y, colpart, Spart, Mpart, cvec, bar, scal, ghist, upd, lapw, permd;
+  DevBuf rcolpart, rbvec, rflags, rdbg;   // on-chip-resident SDSN (K4r)
   DevBuf stA, stB, stK, stX0, stX;
   DevBuf scan;
   double* hscal = nullptr;          // pinned readback
@@ -152,8 +155,14 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
   CK(h->UT.ensure(nn * op_size(op)), "alloc U");
   CK(h->Y.ensure(nn * (f64 ? 8 : 4)), "alloc G/Y");
   CK(h->colpart.ensure((size_t)G * ld * (f64 ? 8 : 4)), "alloc colpart");
-  CK(h->Spart.ensure((size_t)G * 8), "alloc Spart");
-  CK(h->Mpart.ensure((size_t)G * 8), "alloc Mpart");
+  CK(h->Spart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Spart");
+  CK(h->Mpart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Mpart");
+  if (!f64 && fram::sdsn_res_grid(n, h->num_sms) > 0) {
+    const size_t ns = (size_t)fram::sdsn_res_slots(n);
+    CK(h->rcolpart.ensure((size_t)h->num_sms * ns * 4), "alloc resident colpart");
+    CK(h->rbvec.ensure(ns * 4), "alloc resident b");
+    CK(h->rflags.ensure((size_t)h->num_sms * 4), "alloc resident flags");
+  }
   CK(h->cvec.ensure((size_t)ld * 8), "alloc cvec");
   CK(h->bar.ensure(64), "alloc bar");
   CK(h->scal.ensure(kScalDoubles * 8), "alloc scal");
@@ -220,7 +229,53 @@ fram_status gradient(fram_ctx* h, int op, bool haveK, cudaStream_t st) {
   return FRAM_OK;
 }
 
+bool use_resident(const fram_ctx* h, bool f64) {
+  static const bool force_stream = getenv("FRAM_SDSN_STREAM") != nullptr;
+  return !f64 && !force_stream && fram::sdsn_res_grid(h->n, h->num_sms) > 0;
+}
+
 fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
+  double* scal = h->scal.as<double>();
+  if (use_resident(h, f64)) {
+    fram::ResParams r{};
+    r.Y = h->Y.as<float>();
+    r.n = h->n;
+    r.ld = h->ld;
+    r.theta = h->sched.theta;
+    r.gamma_th = h->sched.gamma_th;
+    r.sdsn_max = h->sched.sdsn_max;
+    r.sdsn_fixed = fixed;
+    r.scale = (h->sched.flags & FRAM_FLAG_NO_THETA_SCALE) ? 0 : 1;
+    r.colpart = h->rcolpart.as<float>();
+    r.bvec = h->rbvec.as<float>();
+    r.Spart = h->Spart.as<double>();
+    r.Mpart = h->Mpart.as<double>();
+    r.flags = h->rflags.as<unsigned>();
+    r.passes_out = reinterpret_cast<int*>(scal + 8);
+    r.gamma_hist = h->ghist.as<double>();
+    r.sdsn_out = scal;
+    static const bool timing = getenv("FRAM_RES_TIMING") != nullptr;
+    if (timing) {
+      CK(h->rdbg.ensure((size_t)h->num_sms * 8 * 8), "alloc dbg");
+      r.dbg = h->rdbg.as<long long>();
+    }
+    CK(fram::launch_sdsn_resident(r, st, h->num_sms), "sdsn (on-chip) launch");
+    if (timing) {
+      std::vector<long long> d((size_t)h->num_sms * 8);
+      CK(cudaMemcpyAsync(d.data(), r.dbg, d.size() * 8, cudaMemcpyDeviceToHost, st), "dbg");
+      CK(cudaStreamSynchronize(st), "dbg sync");
+      const int G = fram::sdsn_res_grid(h->n, h->num_sms);
+      double mx[6] = {0};
+      for (int bb = 0; bb < G; ++bb)
+        for (int k = 0; k < 6; ++k) mx[k] = std::max(mx[k], (double)d[bb * 8 + k]);
+      const double np = std::max(1.0, (double)d[5]);
+      fprintf(stderr, "[res timing n=%ld G=%d passes=%.0f] ns/pass (CTA0): bload %.0f sweep %.0f barA %.0f slice %.0f barB %.0f | max over CTAs: %.0f %.0f %.0f %.0f %.0f\n",
+              (long)h->n, G, np, d[0] / np, d[1] / np, d[2] / np, d[3] / np, d[4] / np, mx[0] / np, mx[1] / np, mx[2] / np,
+              mx[3] / np, mx[4] / np);
+    }
+    h->launches += 2;   // flag memset + kernel
+    return FRAM_OK;
+  }
   fram::SdsnParams p{};
   p.Y = h->Y.p;
   p.n = h->n;
@@ -235,7 +290,6 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
   p.Mpart = h->Mpart.as<double>();
   p.cvec = h->cvec.as<double>();
   p.bar = h->bar.as<unsigned>();
-  double* scal = h->scal.as<double>();
   p.passes_out = reinterpret_cast<int*>(scal + 8);
   p.gamma_hist = h->ghist.as<double>();
   p.sdsn_out = scal;
@@ -293,7 +347,7 @@ void fram_destroy(fram_handle h) {
   cudaSetDevice(h->device);
   DevBuf* bufs[] = {&h->Aq, &h->BqT, &h->Kq, &h->N, &h->Nq, &h->UT, &h->Y, &h->colpart, &h->Spart, &h->Mpart,
                     &h->cvec, &h->bar, &h->scal, &h->ghist, &h->upd, &h->lapw, &h->permd, &h->stA, &h->stB,
-                    &h->stK, &h->stX0, &h->stX, &h->scan};
+                    &h->stK, &h->stX0, &h->stX, &h->scan, &h->rcolpart, &h->rbvec, &h->rflags, &h->rdbg};
   for (DevBuf* b : bufs) b->release();
   if (h->hscal) cudaFreeHost(h->hscal);
   for (auto& e : h->ev)

@@ -26,6 +26,28 @@ cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_
 int sdsn_grid_for(long n, int num_sms);
 bool sdsn_supported(long n, bool f64);
 
+// ---- K4r: SDSN with the iterate resident on chip (TMEM + shared memory), FP32, n ≤ ~4.2k ----
+struct ResParams {
+  float* Y;            // n×ld FP32: in X (G), out D (written back after the last pass)
+  long n, ld;
+  double theta, gamma_th;
+  int sdsn_max, sdsn_fixed, scale;
+  float* colpart;      // [grid][slots] per-CTA column partials (slot layout)
+  float* bvec;         // [slots] b_j = −c_j/n (slot layout; −∞ on padding)
+  double* Spart;       // [grid]
+  double* Mpart;       // [grid]
+  unsigned* flags;     // [grid] barrier epochs (zeroed by the launcher)
+  int* passes_out;
+  double* gamma_hist;  // nullable
+  double* sdsn_out;    // [4] as SdsnParams
+  int rs;              // rows per CTA held in shared memory (set by the launcher)
+  int rmax;            // rows per CTA upper bound (set by the launcher)
+  long long* dbg;      // dev-only (FRAM_RES_TIMING): per-CTA phase times [grid][8], nullable
+};
+int sdsn_res_grid(long n, int num_sms);       // 0 ⇒ n not supported on chip
+long sdsn_res_slots(long n);
+cudaError_t launch_sdsn_resident(const ResParams& p, cudaStream_t st, int num_sms);
+
 // ---- K1: preconditioning (Alg.1 steps 2-3) ------------------------------------
 // in_dt: 0 f64, 1 f32, 2 bf16.  op: 0 f64, 1 tf32 (stored f32), 2 bf16, 3 fp16.
 struct PrecondScan {        // device-side result of the validation / max scan

@@ -133,3 +133,20 @@ def test_sdsn_deterministic():
     D1, k1, _ = fram_sdsn(h, X, "fp32")
     D2, k2, _ = fram_sdsn(h, X, "fp32")
     assert k1 == k2 and torch.equal(D1, D2)
+
+
+@pytest.mark.parametrize("n", [33, 129, 777, 1500, 2048, 3000, 4096])
+def test_sdsn_fp32_onchip_sizes(n):
+    # FP32 SDSN at the sizes that select each on-chip layout (K4r: 4/8/16/32 columns per owner
+    # thread, rows in TMEM only or TMEM + shared memory, ragged column tails), a fixed pass count
+    # so the oracle stays cheap; same tolerance model as test_sdsn_fp32_parity.
+    X = random_nonneg(_rng(31 + n), n, "sparse").astype(np.float32)
+    X[0, 0] = max(X[0, 0], 0.5)
+    k = 40
+    h = fram_create(n, schedule=Schedule(theta=10.0, sdsn_fixed=k))
+    D, kk, gam = fram_sdsn(h, _gpu(X, torch.float32), "fp32")
+    assert kk == k
+    Dr, _, go = oracle.sdsn(X.astype(np.float64), 10.0, sdsn_fixed=k, return_gammas=True)
+    tol = 16 * k * U32 * 5.0
+    assert np.max(np.abs(D.cpu().numpy().astype(np.float64) - Dr)) <= tol
+    assert np.max(np.abs(np.array(gam[:k]) - np.array(go[:k]))) <= 1e-4
