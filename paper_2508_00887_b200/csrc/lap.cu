@@ -7,31 +7,52 @@
 //     to the lowest j — the sequential strict-< scan's choice.
 // One CTA of up to 1024 threads.  Column j is owned by thread (j−1) mod THREADS for the whole solve:
 // its minv[j], v[j], used[j] and (once used) p[j] live in that thread's REGISTERS, so a Dijkstra
-// step is one coalesced read of row i0 of N, a register scan, a warp-shuffle argmin, ONE
-// __syncthreads (per-warp candidates double-buffered by step parity; every warp then reduces the
-// candidates itself) and register/shared potential updates.  Row potentials u[], the assignment
+// step is one coalesced read of row i0 of N (issued before the previous step's potential updates),
+// a register scan, a warp argmin by three redux.sync on an order-preserving key, ONE __syncthreads
+// (per-warp candidates double-buffered by step parity; every warp then reduces the candidates
+// itself) and register/shared potential updates.  Row potentials u[], the assignment
 // p[] and way[] live in shared memory (global workspace when n is too large).  u[i0] can be read
 // without a second barrier because the row about to enter the tree is never updated in the step
 // that selects it.
 #include <math_constants.h>
+#include <type_traits>
+#include <stdio.h>
+#include <stdlib.h>
 #include "common.cuh"
 #include "internal.h"
 
 namespace fram {
 namespace {
 
-__device__ __forceinline__ void argmin_merge(double& v, int& j, double ov, int oj) {
-  if (ov < v || (ov == v && oj < j)) { v = ov; j = oj; }
+// Order-preserving map FP64 → uint64 (negative: flip all bits; non-negative: flip the sign bit),
+// so that unsigned comparison of keys equals numeric comparison of the doubles (no NaN here).
+__device__ __forceinline__ uint64_t okey(double x) {
+  const uint64_t b = (uint64_t)__double_as_longlong(x);
+  return b ^ ((b >> 63) ? 0xffffffffffffffffull : 0x8000000000000000ull);
+}
+__device__ __forceinline__ double unkey(uint64_t k) {
+  const uint64_t b = k ^ ((k >> 63) ? 0x8000000000000000ull : 0xffffffffffffffffull);
+  return __longlong_as_double((long long)b);
+}
+// Warp argmin over (key, j): lexicographic — the smallest value, ties to the lowest column j
+// (the sequential strict-< scan's choice, R17).  Three redux.sync instead of a shuffle tree.
+__device__ __forceinline__ void warp_argmin(uint64_t& key, int& j) {
+  const unsigned hi = (unsigned)(key >> 32), lo = (unsigned)key;
+  const unsigned mhi = __reduce_min_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_min_sync(0xffffffffu, hi == mhi ? lo : 0xffffffffu);
+  const bool win = (hi == mhi) && (lo == mlo);
+  j = (int)__reduce_min_sync(0xffffffffu, win ? (unsigned)j : 0x7fffffffu);
+  key = ((uint64_t)mhi << 32) | mlo;
 }
 
-template <int THREADS, int CPT>
+template <int THREADS, int CPT, bool SMEM>
 __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restrict__ N, int n, long ld,
-                                                         int32_t* perm, void* gwork, int use_smem) {
+                                                         int32_t* perm, void* gwork) {
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ double s_v[2][WARPS];                    // per-warp argmin candidates, double-buffered
+  __shared__ uint64_t s_k[2][WARPS];                  // per-warp argmin candidates, double-buffered
   __shared__ int s_j[2][WARPS];                       // by step parity (one barrier per step)
-  unsigned char* base = use_smem ? dsm : reinterpret_cast<unsigned char*>(gwork);
+  unsigned char* base = SMEM ? dsm : reinterpret_cast<unsigned char*>(gwork);
   const int m = n + 1;
   double* u = reinterpret_cast<double*>(base);        // row potentials u[0..n]
   int* p = reinterpret_cast<int*>(u + m);             // p[j]: row owning column j (0 = free)
@@ -39,76 +60,81 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // column j = 1 + tid + k·THREADS lives in this thread's registers
-  double minv[CPT], v[CPT];
+  double minv[CPT], v[CPT], cv[CPT];
   int prow[CPT];                                      // row owning a USED column (fixed during a search)
+  using Mask = typename std::conditional<(CPT > 32), uint64_t, uint32_t>::type;
+  constexpr Mask one = 1;
+  Mask inr = 0;                                       // bit k: column j ≤ n exists
 #pragma unroll
-  for (int k = 0; k < CPT; ++k) { v[k] = 0.0; prow[k] = 0; }
+  for (int k = 0; k < CPT; ++k) {
+    v[k] = 0.0;
+    prow[k] = 0;
+    if (1 + tid + k * THREADS <= n) inr |= one << k;
+  }
   for (int j = tid; j < m; j += THREADS) { u[j] = 0.0; p[j] = 0; way[j] = 0; }
   __syncthreads();
 
+  auto load_row = [&](int row) {                      // row `row` (1-based) of N into cv[]
+    const double* crow = N + (long)(row - 1) * ld + tid;
+#pragma unroll
+    for (int k = 0; k < CPT; ++k) cv[k] = ((inr >> k) & one) ? __ldcg(crow + k * THREADS) : 0.0;
+  };
+
   int par = 0;
   for (int i = 1; i <= n; ++i) {
-    uint64_t used = 0;
+    Mask fr = inr;                                    // bit k: column free (not yet in the tree)
 #pragma unroll
     for (int k = 0; k < CPT; ++k) minv[k] = CUDART_INF;
     if (tid == 0) p[0] = i;                           // read only by thread 0's augmentation
     int j0 = 0, i0 = i;
+    load_row(i0);
     while (true) {
       // used[j0] = true (the owner remembers p[j0] = i0 for the potential updates)
       if (j0 > 0 && ((j0 - 1) % THREADS) == tid) {
         const int kk = (j0 - 1) / THREADS;
-        used |= 1ull << kk;
+        fr &= ~(one << kk);
 #pragma unroll
-        for (int k = 0; k < CPT; ++k)
-          if (k == kk) prow[k] = i0;
+        for (int k = 0; k < CPT; ++k) prow[k] = (k == kk) ? i0 : prow[k];
       }
       const double ui0 = u[i0];                       // not written during this step (i0 ∉ tree)
-      const double* crow = N + (long)(i0 - 1) * ld;
-      double cv[CPT];
-#pragma unroll
-      for (int k = 0; k < CPT; ++k) {
-        const int j = 1 + tid + k * THREADS;
-        cv[k] = (j <= n) ? __ldcg(crow + (j - 1)) : 0.0;
-      }
       double best = CUDART_INF;
       int bj = 0x7fffffff;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {                 // k ascending ⇒ j ascending: strict < keeps lowest j
-        const int j = 1 + tid + k * THREADS;
-        if (j <= n && !((used >> k) & 1ull)) {
-          const double cur = __dsub_rn(__dsub_rn(-cv[k], ui0), v[k]);   // (C[i0][j] − u[i0]) − v[j]
-          if (cur < minv[k]) { minv[k] = cur; way[j] = j0; }
-          if (minv[k] < best) { best = minv[k]; bj = j; }
-        }
+        const bool f = (fr >> k) & one;
+        const double cur = __dsub_rn(__dsub_rn(-cv[k], ui0), v[k]);     // (C[i0][j] − u[i0]) − v[j]
+        const bool upd = f && cur < minv[k];
+        minv[k] = upd ? cur : minv[k];
+        if (upd) way[1 + tid + k * THREADS] = j0;
+        const bool bt = f && minv[k] < best;
+        best = bt ? minv[k] : best;
+        bj = bt ? 1 + tid + k * THREADS : bj;
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)
-        argmin_merge(best, bj, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, bj, o));
-      if (lane == 0) { s_v[par][warp] = best; s_j[par][warp] = bj; }
+      uint64_t key = okey(best);
+      warp_argmin(key, bj);
+      if (lane == 0) { s_k[par][warp] = key; s_j[par][warp] = bj; }
       __syncthreads();
       // every warp reduces the WARPS candidates itself (no second barrier)
-      double delta = (lane < WARPS) ? s_v[par][lane] : CUDART_INF;
+      uint64_t dkey = (lane < WARPS) ? s_k[par][lane] : ~0ull;
       int j1 = (lane < WARPS) ? s_j[par][lane] : 0x7fffffff;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1)                // lanes ≥ WARPS hold +inf: all lanes converge
-        argmin_merge(delta, j1, __shfl_xor_sync(0xffffffffu, delta, o), __shfl_xor_sync(0xffffffffu, j1, o));
+      warp_argmin(dkey, j1);
+      const double delta = unkey(dkey);
       par ^= 1;
+      const int i0n = p[j1];                          // p is not modified during a search
+      if (i0n != 0) load_row(i0n);                    // next row's loads overlap the updates below
       // potentials: used columns (u[p[j]] += δ, v[j] −= δ), virtual column 0 (u[i] += δ), free minv −= δ
+      const Mask usd = inr & ~fr;
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
-        const int j = 1 + tid + k * THREADS;
-        if (j <= n) {
-          if ((used >> k) & 1ull) {
-            u[prow[k]] = __dadd_rn(u[prow[k]], delta);
-            v[k] = __dsub_rn(v[k], delta);
-          } else {
-            minv[k] = __dsub_rn(minv[k], delta);
-          }
+        if ((usd >> k) & one) {
+          u[prow[k]] = __dadd_rn(u[prow[k]], delta);
+          v[k] = __dsub_rn(v[k], delta);
         }
+        minv[k] = ((fr >> k) & one) ? __dsub_rn(minv[k], delta) : minv[k];
       }
       if (tid == 0) u[i] = __dadd_rn(u[i], delta);
       j0 = j1;
-      i0 = p[j1];                                     // p is not modified during a search
+      i0 = i0n;
       if (i0 == 0) break;
     }
     __syncthreads();                                  // all reads of p / writes of way and u done
@@ -128,13 +154,14 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
 template <int THREADS, int CPT>
 cudaError_t launch_t(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
   const size_t bytes = lap_work_bytes(n);
-  const bool smem = bytes <= 200 * 1024;
-  auto fn = lap_kernel<THREADS, CPT>;
-  if (smem) {
+  if (bytes <= 200 * 1024) {
+    auto fn = lap_kernel<THREADS, CPT, true>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
+    fn<<<1, THREADS, bytes, st>>>(N, (int)n, ld, perm, work);
+  } else {
+    lap_kernel<THREADS, CPT, false><<<1, THREADS, 0, st>>>(N, (int)n, ld, perm, work);
   }
-  fn<<<1, THREADS, smem ? bytes : 0, st>>>(N, (int)n, ld, perm, work, smem ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -145,9 +172,14 @@ size_t lap_work_bytes(long n) { return (size_t)(n + 1) * (sizeof(double) + 2 * s
 cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
   if (n <= 256) return launch_t<256, 1>(N, n, ld, perm, work, st);
   if (n <= 512) return launch_t<512, 1>(N, n, ld, perm, work, st);
-  if (n <= 1024) return launch_t<1024, 1>(N, n, ld, perm, work, st);
-  if (n <= 2048) return launch_t<1024, 2>(N, n, ld, perm, work, st);
-  if (n <= 4096) return launch_t<1024, 4>(N, n, ld, perm, work, st);
+  if (n <= 1024) return launch_t<512, 2>(N, n, ld, perm, work, st);
+  if (n <= 2048) return launch_t<512, 4>(N, n, ld, perm, work, st);
+  if (n <= 4096) {
+    static const int cfg = getenv("FRAM_LAP_CFG") ? atoi(getenv("FRAM_LAP_CFG")) : 512;   // dev knob
+    if (cfg == 256) return launch_t<256, 16>(N, n, ld, perm, work, st);
+    if (cfg == 1024) return launch_t<1024, 4>(N, n, ld, perm, work, st);
+    return launch_t<512, 8>(N, n, ld, perm, work, st);
+  }
   if (n <= 8192) return launch_t<1024, 8>(N, n, ld, perm, work, st);
   if (n <= 16384) return launch_t<1024, 16>(N, n, ld, perm, work, st);
   if (n <= 65536) return launch_t<1024, 64>(N, n, ld, perm, work, st);
