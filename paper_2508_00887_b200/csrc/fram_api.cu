@@ -158,10 +158,7 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
   CK(h->Spart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Spart");
   CK(h->Mpart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Mpart");
   if (!f64 && fram::sdsn_res_grid(n, h->num_sms) > 0) {
-    const size_t ns = (size_t)fram::sdsn_res_slots(n);
-    CK(h->rcolpart.ensure((size_t)h->num_sms * ns * 4), "alloc resident colpart");
-    CK(h->rbvec.ensure(ns * 4), "alloc resident b");
-    CK(h->rflags.ensure((size_t)h->num_sms * 4), "alloc resident flags");
+    CK(h->rcolpart.ensure(fram::sdsn_res_xchg_words(n, h->num_sms) * 8), "alloc resident exchange");
   }
   CK(h->cvec.ensure((size_t)ld * 8), "alloc cvec");
   CK(h->bar.ensure(64), "alloc bar");
@@ -246,15 +243,13 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
     r.sdsn_max = h->sched.sdsn_max;
     r.sdsn_fixed = fixed;
     r.scale = (h->sched.flags & FRAM_FLAG_NO_THETA_SCALE) ? 0 : 1;
-    r.colpart = h->rcolpart.as<float>();
-    r.bvec = h->rbvec.as<float>();
-    r.Spart = h->Spart.as<double>();
-    r.Mpart = h->Mpart.as<double>();
-    r.flags = h->rflags.as<unsigned>();
+    r.xchg = h->rcolpart.as<uint64_t>();
     r.passes_out = reinterpret_cast<int*>(scal + 8);
     r.gamma_hist = h->ghist.as<double>();
     r.sdsn_out = scal;
     static const bool timing = getenv("FRAM_RES_TIMING") != nullptr;
+    static const int dbgmode = getenv("FRAM_RES_DBGMODE") ? atoi(getenv("FRAM_RES_DBGMODE")) : 0;
+    r.dbgmode = dbgmode;
     if (timing) {
       CK(h->rdbg.ensure((size_t)h->num_sms * 8 * 8), "alloc dbg");
       r.dbg = h->rdbg.as<long long>();
@@ -269,9 +264,9 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
       for (int bb = 0; bb < G; ++bb)
         for (int k = 0; k < 6; ++k) mx[k] = std::max(mx[k], (double)d[bb * 8 + k]);
       const double np = std::max(1.0, (double)d[5]);
-      fprintf(stderr, "[res timing n=%ld G=%d passes=%.0f] ns/pass (CTA0): bload %.0f sweep %.0f barA %.0f slice %.0f barB %.0f | max over CTAs: %.0f %.0f %.0f %.0f %.0f\n",
-              (long)h->n, G, np, d[0] / np, d[1] / np, d[2] / np, d[3] / np, d[4] / np, mx[0] / np, mx[1] / np, mx[2] / np,
-              mx[3] / np, mx[4] / np);
+      fprintf(stderr, "[res timing n=%ld G=%d passes=%.0f] ns/pass (CTA0): bload %.0f sweep %.0f [spart %.0f stores %.0f srows %.0f sync %.0f] slice %.0f | max over CTAs: %.0f %.0f %.0f\n",
+              (long)h->n, G, np, d[0] / np, d[1] / np, d[2] / np, d[4] / np, d[6] / np, d[7] / np, d[3] / np, mx[0] / np, mx[1] / np,
+              mx[3] / np);
     }
     h->launches += 2;   // flag memset + kernel
     return FRAM_OK;

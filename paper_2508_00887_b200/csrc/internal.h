@@ -32,20 +32,22 @@ struct ResParams {
   long n, ld;
   double theta, gamma_th;
   int sdsn_max, sdsn_fixed, scale;
-  float* colpart;      // [grid][slots] per-CTA column partials (slot layout)
-  float* bvec;         // [slots] b_j = −c_j/n (slot layout; −∞ on padding)
-  double* Spart;       // [grid]
-  double* Mpart;       // [grid]
-  unsigned* flags;     // [grid] barrier epochs (zeroed by the launcher)
+  uint64_t* xchg;      // tagged exchange words (zeroed by the launcher), see sdsn_res_xchg_words
+  unsigned* colpart;   // [grid][slots]   per-CTA column partials (slot layout), parity bit | fp32
+  unsigned* bvec;      // [slots]         |b_j| = c_j/n (∞ on padding), parity bit | fp32
+  uint64_t* Spart;     // [2][grid]       per-CTA Σ row sums (FP64, tag in the sign bit), by epoch parity
+  uint64_t* Mpart;     // [grid]          per-CTA max (FP64, tag in the sign bit)
   int* passes_out;
   double* gamma_hist;  // nullable
   double* sdsn_out;    // [4] as SdsnParams
   int rs;              // rows per CTA held in shared memory (set by the launcher)
   int rmax;            // rows per CTA upper bound (set by the launcher)
   long long* dbg;      // dev-only (FRAM_RES_TIMING): per-CTA phase times [grid][8], nullable
+  int dbgmode;         // dev-only (FRAM_RES_DBGMODE): 1 skip SMEM rows, 2 skip TMEM rows (timing only)
 };
 int sdsn_res_grid(long n, int num_sms);       // 0 ⇒ n not supported on chip
 long sdsn_res_slots(long n);
+size_t sdsn_res_xchg_words(long n, int num_sms);   // size of ResParams::xchg
 cudaError_t launch_sdsn_resident(const ResParams& p, cudaStream_t st, int num_sms);
 
 // ---- K1: preconditioning (Alg.1 steps 2-3) ------------------------------------

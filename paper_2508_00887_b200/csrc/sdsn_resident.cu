@@ -35,8 +35,7 @@
 namespace fram {
 namespace {
 
-constexpr int kResThreads = 256;             // 8 warps = 4 TMEM lane quarters × 2 row groups
-constexpr int kResSmemMax = 232448 - 2304;   // 227 KB opt-in minus static shared memory (2128 B)
+constexpr int kResSmemMax = 232448 - 4608;   // 227 KB opt-in minus static shared memory (≤ 4.3 KB)
 constexpr int kResMinSmem = 120 * 1024;      // forces one CTA per SM (TMEM: 512 columns per CTA)
 
 template <int CPT> struct RC {
@@ -51,7 +50,72 @@ constexpr int kResKMax = 5;                  // G ≤ 32·kResKMax CTAs (148 SMs
 // dynamic shared memory: SMEM-resident rows, column staging, per-thread row partials, s_r, s_a
 size_t res_smem_bytes(int cpt, int rs, int R) {
   const size_t ns = 128 * (size_t)cpt;
-  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 128 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
+  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 8 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
+}
+
+__device__ __forceinline__ uint64_t tag_f(float v, unsigned e) {
+  return ((uint64_t)e << 32) | __float_as_uint(v);
+}
+__device__ __forceinline__ unsigned tag_of(uint64_t w) { return (unsigned)(w >> 32); }
+__device__ __forceinline__ float val_f(uint64_t w) { return __uint_as_float((unsigned)w); }
+__device__ __forceinline__ uint64_t ld_tag(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_tag(uint64_t* p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_tag2(uint64_t* p, uint64_t a, uint64_t b) {   // 16-B aligned pair
+  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+__device__ __forceinline__ void ld_tag2(const uint64_t* p, uint64_t& a, uint64_t& b) {
+  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
+}
+// an FP64 value published as two tagged words (hi, lo halves)
+__device__ __forceinline__ void st_tag_d(uint64_t* p, double v, unsigned e) {
+  const uint64_t bits = (uint64_t)__double_as_longlong(v);
+  st_tag2(p, ((uint64_t)e << 32) | (bits >> 32), ((uint64_t)e << 32) | (bits & 0xffffffffull));
+}
+__device__ __forceinline__ double wait_tag_d(const uint64_t* p, unsigned e) {
+  uint64_t hi, lo;
+  do { ld_tag2(p, hi, lo); } while (tag_of(hi) != e || tag_of(lo) != e);
+  return __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
+}
+
+// 32-bit words: a non-negative FP32 magnitude with the epoch parity in the (otherwise zero) sign bit.
+// A slot read for epoch e can only hold epoch e−1 or e (see the ordering argument in the kernel),
+// so one bit distinguishes them.
+__device__ __forceinline__ unsigned ptag(float mag, unsigned e) { return __float_as_uint(mag) | ((e & 1u) << 31); }
+__device__ __forceinline__ bool pok(unsigned w, unsigned e) { return (w >> 31) == (e & 1u); }
+__device__ __forceinline__ float pval(unsigned w) { return __uint_as_float(w & 0x7fffffffu); }
+__device__ __forceinline__ unsigned ld_w(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 ld_w4(const unsigned* p) {
+  uint4 v;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_w(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_w4(unsigned* p, uint4 v) {
+  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+// a non-negative FP64 value with a 1-bit tag in the sign bit (one single-copy-atomic 8-byte word)
+__device__ __forceinline__ void st_d1(uint64_t* p, double v, unsigned bit) {
+  const uint64_t w = (uint64_t)__double_as_longlong(v) | ((uint64_t)bit << 63);
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+__device__ __forceinline__ double wait_d1(const uint64_t* p, unsigned bit) {
+  uint64_t w;
+  do { w = ld_tag(p); } while ((unsigned)(w >> 63) != bit);
+  return __longlong_as_double((long long)(w & 0x7fffffffffffffffull));
 }
 
 // two FP32 adds in one instruction (FADD2, sm_100): d = (a.x + b.x, a.y + b.y), each RN
@@ -64,31 +128,46 @@ __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   return d;
 }
 
+// Threads: warp w → TMEM lane quarter q = w%4, column half h (SPLIT only), row group g.
+// Thread (q, lane, h) owns columns [t·CPT + h·CH, +CH) of every row, t = 32q + lane, CH = CPT/NH.
+template <int CPT> struct RK {
+  static constexpr bool SPLIT = CPT >= 8;                // two warps share each TMEM lane's row slice
+  static constexpr int NH = SPLIT ? 2 : 1;
+  static constexpr int THREADS = SPLIT ? 512 : 256;
+  static constexpr int NW = THREADS / 32;
+  static constexpr int CH = CPT / NH;                    // columns per thread
+  static constexpr int VH = CH / 4;                      // float4 chunks per thread per row
+};
+
 template <int CPT>
-__global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
+__global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams P) {
   using C = RC<CPT>;
+  using K = RK<CPT>;
   constexpr int V = C::V, NS = C::NS, RT = C::RT;
+  constexpr int NW = K::NW, CH = K::CH, VH = K::VH, THREADS = K::THREADS;
   extern __shared__ __align__(16) unsigned char dsm[];
   const int RS = P.rs;
   const int Rmax = P.rmax;
   float4* s_rows = reinterpret_cast<float4*>(dsm);                    // [RS][V·128] slot layout
   float4* s_col = s_rows + (size_t)RS * V * 128;                      // [V·128] column staging
-  float* s_rowthr = reinterpret_cast<float*>(s_col + V * 128);        // [Rmax][128] per-thread row partials
-  double* s_r = reinterpret_cast<double*>(s_rowthr + Rmax * 128);    // [Rmax] row sums (FP64)
+  float* s_rowpart = reinterpret_cast<float*>(s_col + V * 128);       // [Rmax][8] per-warp row partials
+  double* s_r = reinterpret_cast<double*>(s_rowpart + Rmax * 8);     // [Rmax] row sums (FP64)
   float* s_a = reinterpret_cast<float*>(s_r + Rmax);                 // [Rmax] a_i (FP32)
   __shared__ uint32_t s_tmem;
-  __shared__ double s_red[kResThreads / 32];
+  __shared__ double s_red[NW];
   __shared__ double s_S;
-  __shared__ double s_red2[kResThreads / 32][32];
+  __shared__ double s_red2[NW][32];
 
   const int G = gridDim.x, b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = warp & 3, g = warp >> 2;
+  const int q = warp & 3;
+  const int h = K::SPLIT ? (warp >> 2) & 1 : 0;
+  const int g = K::SPLIT ? warp >> 3 : warp >> 2;
   const int t = q * 32 + lane;
+  const int c0 = h * VH;                                 // first float4 chunk of this thread
   const long n = P.n, ld = P.ld;
   const long r0 = (long)b * n / G, r1 = (long)(b + 1) * n / G;
   const int R = (int)(r1 - r0);
   const double dn = (double)n, nn = dn * dn;
-  unsigned epoch = 0;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -98,50 +177,41 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = s_tmem + ((uint32_t)(q * 32) << 16);          // this warp's lane quarter
+  const uint32_t tmem = s_tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * CH);   // lane quarter, half
 
-  auto load_row = [&](int r, float (&x)[CPT]) {
+  auto load_row = [&](int r, float (&x)[CH]) {
     if (r < RT) {
-      uint32_t v[CPT];
-      tmem_ld<CPT>(tmem + (uint32_t)(r * CPT), v);
+      uint32_t v[CH];
+      tmem_ld<CH>(tmem + (uint32_t)(r * CPT), v);
       tmem_wait_ld();
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) x[k] = __uint_as_float(v[k]);
+      for (int k = 0; k < CH; ++k) x[k] = __uint_as_float(v[k]);
     } else {
       const float4* row = s_rows + (size_t)(r - RT) * (V * 128);
 #pragma unroll
-      for (int c = 0; c < V; ++c) {
-        const float4 v = row[c * 128 + t];
+      for (int c = 0; c < VH; ++c) {
+        const float4 v = row[(c0 + c) * 128 + t];
         x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
       }
     }
   };
-  auto store_row = [&](int r, const float (&x)[CPT]) {
+  auto store_row = [&](int r, const float (&x)[CH]) {
     if (r < RT) {
-      uint32_t v[CPT];
+      uint32_t v[CH];
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) v[k] = __float_as_uint(x[k]);
-      tmem_st<CPT>(tmem + (uint32_t)(r * CPT), v);
+      for (int k = 0; k < CH; ++k) v[k] = __float_as_uint(x[k]);
+      tmem_st<CH>(tmem + (uint32_t)(r * CPT), v);
     } else {
       float4* row = s_rows + (size_t)(r - RT) * (V * 128);
 #pragma unroll
-      for (int c = 0; c < V; ++c) row[c * 128 + t] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+      for (int c = 0; c < VH; ++c)
+        row[(c0 + c) * 128 + t] = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
     }
   };
-  // grid-wide barrier: one monotonic arrival counter (red.release), one acquire poller per CTA
-  auto gbar = [&]() {
-    ++epoch;
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(P.flags) : "memory");
-      const unsigned target = epoch * (unsigned)G;
-      unsigned v;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(P.flags) : "memory");
-      } while (v < target);
-    }
-    __syncthreads();
-  };
+  // Cross-CTA exchange without grid barriers: every published value travels in one 8-byte word
+  // together with the epoch it belongs to (single-copy atomic), and a consumer re-reads a word
+  // until its tag matches — it waits for exactly the data it needs.  Tags are zeroed by the
+  // launcher; epochs start at 1.
   auto dealloc = [&]() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -153,10 +223,10 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
     float lmax = 0.f;
     for (int r = g; r < R; r += 2) {
       const float* grow = P.Y + (r0 + r) * ld;
-      float x[CPT];
+      float x[CH];
 #pragma unroll
-      for (int c = 0; c < V; ++c) {
-        const long col = (long)t * CPT + 4 * c;
+      for (int c = 0; c < VH; ++c) {
+        const long col = (long)t * CPT + 4 * (c0 + c);
         float4 v;
         if (col + 3 < n) {
           v = __ldcg(reinterpret_cast<const float4*>(grow + col));
@@ -178,19 +248,17 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
     __syncthreads();
     if (tid == 0) {
       double mm = 0.0;
-      for (int w = 0; w < kResThreads / 32; ++w) mm = fmax(mm, s_red[w]);
-      P.Mpart[b] = mm;
+      for (int w = 0; w < NW; ++w) mm = fmax(mm, s_red[w]);
+      st_d1(P.Mpart + b, mm, 1u);
     }
   }
   double sc = 1.0;
   if (P.scale) {
-    gbar();
     if (warp == 0) {
-      double mv[kResKMax], mm = 0.0;
+      double mm = 0.0;
 #pragma unroll
-      for (int i = 0; i < kResKMax; ++i) mv[i] = (lane + 32 * i < G) ? __ldcg(P.Mpart + lane + 32 * i) : 0.0;
-#pragma unroll
-      for (int i = 0; i < kResKMax; ++i) mm = fmax(mm, mv[i]);
+      for (int i = 0; i < kResKMax; ++i)
+        if (lane + 32 * i < G) mm = fmax(mm, wait_d1(P.Mpart + lane + 32 * i, 1u));
       mm = warp_max_d(mm);
       if (lane == 0) s_S = mm;
     }
@@ -199,7 +267,7 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
     if (m == 0.0) {                                      // R10: all-zero ⇒ 11ᵀ/n, 0 passes
       for (int r = g; r < R; r += 2) {
         float* grow = P.Y + (r0 + r) * ld;
-        for (long col = (long)t; col < n; col += 128) grow[col] = (float)(1.0 / dn);
+        for (long col = (long)(h * 128 + t); col < n; col += 128 * K::NH) grow[col] = (float)(1.0 / dn);
       }
       if (b == 0 && tid == 0) {
         *P.passes_out = 0;
@@ -213,83 +281,98 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
     __syncthreads();                                     // s_S is reused below
   }
 
-  // ---------------- one sweep over the CTA's rows ----------------
-  // PASS: y ← max(0, (y + a_i) + b_j);  SCALE: y ← fl(s·y).  Accumulates the new row sums
-  // (s_r, Spart[b]) and column partials (colpart[b], slot layout).
   // after a sweep: column partials (two row groups combined in shared memory) → colpart[b];
-  // row sums (per-thread partials → fixed-order tree) → s_r; Σ r → Spart[b]
-  auto sweep_epilogue = [&](const float (&col)[CPT]) {
+  // row sums (per-lane partials → fixed-order tree) → s_r; Σ r → Spart[b]; all tagged e
+  long long tfine[4] = {0, 0, 0, 0};
+  auto gt = [&]() -> long long {
+    long long v = 0;
+    if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    return v;
+  };
+  auto sweep_epilogue = [&](const float (&col)[CH], unsigned e) {
+    const long long e0 = gt();
     tmem_wait_st();
     if (g == 1) {
 #pragma unroll
-      for (int c = 0; c < V; ++c) s_col[c * 128 + t] = make_float4(col[4 * c], col[4 * c + 1], col[4 * c + 2], col[4 * c + 3]);
+      for (int c = 0; c < VH; ++c)
+        s_col[(c0 + c) * 128 + t] = make_float4(col[4 * c], col[4 * c + 1], col[4 * c + 2], col[4 * c + 3]);
     }
     __syncthreads();
-    if (g == 0) {
-      float4* dst = reinterpret_cast<float4*>(P.colpart + (long)b * NS);
+    const long long e1 = gt();
+    if (g == 0 && e != 0) {
+      unsigned* dst = P.colpart + (long)b * NS;
 #pragma unroll
-      for (int c = 0; c < V; ++c) {
-        float4 o = s_col[c * 128 + t];
+      for (int c = 0; c < VH; ++c) {
+        float4 o = s_col[(c0 + c) * 128 + t];
         o.x += col[4 * c]; o.y += col[4 * c + 1]; o.z += col[4 * c + 2]; o.w += col[4 * c + 3];
-        __stcg(dst + c * 128 + t, o);
+        st_w4(dst + (size_t)((c0 + c) * 128 + t) * 4, make_uint4(ptag(o.x, e), ptag(o.y, e), ptag(o.z, e), ptag(o.w, e)));
       }
     }
-    // row sums: warp w reduces rows w, w+8, …, up to 4 at a time (independent shuffle chains)
-    for (int r = warp; r < R; r += 4 * (kResThreads / 32)) {
-      float pr[4];
+    const long long e1a = gt();
+    // row sums: the 4·NH per-warp partials of each row, combined in FP64 in a fixed order
+    for (int i = tid; i < R; i += THREADS) {
+      const float* pp = s_rowpart + i * 8;
+      double acc = 0.0;
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int rr = r + u * (kResThreads / 32);
-        const float* pp = s_rowthr + rr * 128;
-        pr[u] = rr < R ? ((pp[lane] + pp[lane + 32]) + (pp[lane + 64] + pp[lane + 96])) : 0.f;
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) pr[u] = warp_sum_f(pr[u]);
-      if (lane == 0) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (r + u * (kResThreads / 32) < R) s_r[r + u * (kResThreads / 32)] = (double)pr[u];
-      }
+      for (int k = 0; k < 4 * K::NH; ++k) acc += (double)pp[k];
+      s_r[i] = acc;
     }
+    const long long e1b = gt();
     __syncthreads();
-    if (warp == 0) {
+    const long long e1c = gt();
+    if (warp == 0 && e != 0) {
       double s = 0.0;
       for (int i = lane; i < R; i += 32) s += s_r[i];
       s = warp_sum_d(s);
-      if (lane == 0) __stcg(P.Spart + b, s);
+      if (lane == 0) st_d1(P.Spart + (size_t)(e & 1) * G + b, s, (e >> 1) & 1u);
+    }
+    const long long e2 = gt();
+    tfine[1] += e1a - e1; tfine[2] += e1b - e1a; tfine[3] += e1c - e1b; tfine[0] += e2 - e1c;
+  };
+  // this warp's partials of rows ra and rb (rb < 0: none): two interleaved shuffle trees, lane 0
+  // stores them at slot 4·h + q of the row (fixed order, deterministic)
+  auto put_rowparts = [&](int ra, float va, int rb, float vb) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      va += __shfl_xor_sync(0xffffffffu, va, o);
+      vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    }
+    if (lane == 0) {
+      s_rowpart[ra * 8 + 4 * h + q] = va;
+      if (rb >= 0) s_rowpart[rb * 8 + 4 * h + q] = vb;
     }
   };
 
   // Y0 = fl(s·X) (Alg.2 step 1; skipped when !P.scale) with its sums
   auto sweep_scale = [&]() {
-    float col[CPT];
+    float col[CH];
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) col[k] = 0.f;
+    for (int k = 0; k < CH; ++k) col[k] = 0.f;
     for (int r = g; r < R; r += 2) {
-      float x[CPT];
+      float x[CH];
       load_row(r, x);
       float r0s = 0.f, r1s = 0.f;
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) {
+      for (int k = 0; k < CH; ++k) {
         const float y = P.scale ? (float)(sc * (double)x[k]) : x[k];
         x[k] = y;
         col[k] += y;
         if (k & 1) r1s += y; else r0s += y;
       }
       if (P.scale) store_row(r, x);
-      s_rowthr[r * 128 + t] = r0s + r1s;
+      put_rowparts(r, r0s + r1s, -1, 0.f);
     }
-    sweep_epilogue(col);
+    sweep_epilogue(col, 1u);
   };
 
-  // one SDSN pass: y ← max(0, (y + a_i) + b_j) (P2∘P1, R9 grouping), two rows at a time with
-  // paired FP32 adds (add.rn.f32x2: x+a, +b, column and row accumulation)
-  auto pass_rows = [&](float (&x)[CPT], float a, const float (&bv)[CPT], float2 (&col2)[CPT / 2]) -> float {
+  // one SDSN pass on one row slice: y ← max(0, (y + a_i) + b_j) (P2∘P1, R9 grouping) with paired
+  // FP32 adds (add.rn.f32x2: x+a, +b, column and row accumulation)
+  auto pass_rows = [&](float (&x)[CH], float a, const float2 (&bv)[CH / 2], float2 (&col2)[CH / 2]) -> float {
     float2 rs = make_float2(0.f, 0.f);
     const float2 a2 = make_float2(a, a);
 #pragma unroll
-    for (int k = 0; k < CPT; k += 2) {
-      float2 y = add2(add2(make_float2(x[k], x[k + 1]), a2), make_float2(bv[k], bv[k + 1]));
+    for (int k = 0; k < CH; k += 2) {
+      float2 y = add2(add2(make_float2(x[k], x[k + 1]), a2), bv[k / 2]);
       y.x = fmaxf(0.0f, y.x);
       y.y = fmaxf(0.0f, y.y);
       x[k] = y.x;
@@ -299,21 +382,24 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
     }
     return rs.x + rs.y;
   };
-  auto sweep_pass = [&](const float (&bv)[CPT]) {
-    float2 col2[CPT / 2];
+  auto sweep_pass = [&](const float2 (&bv)[CH / 2], unsigned e) {
+    const long long l0 = gt();
+    float2 col2[CH / 2];
 #pragma unroll
-    for (int k = 0; k < CPT / 2; ++k) col2[k] = make_float2(0.f, 0.f);
+    for (int k = 0; k < CH / 2; ++k) col2[k] = make_float2(0.f, 0.f);
     int ra = g;
-    for (; ra + 2 < R; ra += 4) {
+    const int Rl = (P.dbgmode & 1) ? min(R, RT) : R;    // dev timing knobs (FRAM_RES_DBGMODE)
+    if (P.dbgmode & 2) ra = g + ((RT - g + 3) / 4) * 4;
+    for (; ra + 2 < Rl; ra += 4) {                       // rows g, g+2, … two at a time
       const int rb = ra + 2;
-      float xa[CPT], xb[CPT];
+      float xa[CH], xb[CH];
       if (rb < RT) {                                     // both rows in TMEM: one wait for two loads
-        uint32_t va[CPT], vb[CPT];
-        tmem_ld<CPT>(tmem + (uint32_t)(ra * CPT), va);
-        tmem_ld<CPT>(tmem + (uint32_t)(rb * CPT), vb);
+        uint32_t va[CH], vb[CH];
+        tmem_ld<CH>(tmem + (uint32_t)(ra * CPT), va);
+        tmem_ld<CH>(tmem + (uint32_t)(rb * CPT), vb);
         tmem_wait_ld();
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) { xa[k] = __uint_as_float(va[k]); xb[k] = __uint_as_float(vb[k]); }
+        for (int k = 0; k < CH; ++k) { xa[k] = __uint_as_float(va[k]); xb[k] = __uint_as_float(vb[k]); }
       } else {
         load_row(ra, xa);
         load_row(rb, xb);
@@ -322,60 +408,66 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
       const float sb = pass_rows(xb, s_a[rb], bv, col2);
       store_row(ra, xa);
       store_row(rb, xb);
-      s_rowthr[ra * 128 + t] = sa;
-      s_rowthr[rb * 128 + t] = sb;
+      put_rowparts(ra, sa, rb, sb);
     }
-    if (ra < R) {
-      float xa[CPT];
+    if (ra < Rl) {
+      float xa[CH];
       load_row(ra, xa);
-      s_rowthr[ra * 128 + t] = pass_rows(xa, s_a[ra], bv, col2);
+      const float sa = pass_rows(xa, s_a[ra], bv, col2);
       store_row(ra, xa);
+      put_rowparts(ra, sa, -1, 0.f);
     }
-    float col[CPT];
+    float col[CH];
 #pragma unroll
-    for (int k = 0; k < CPT / 2; ++k) { col[2 * k] = col2[k].x; col[2 * k + 1] = col2[k].y; }
-    sweep_epilogue(col);
+    for (int k = 0; k < CH / 2; ++k) { col[2 * k] = col2[k].x; col[2 * k + 1] = col2[k].y; }
+    (void)l0;
+    sweep_epilogue(col, e);
   };
 
-  // slot slice b: lane ↔ slot (coalesced rows of colpart), warp ↔ source CTA k ≡ warp (mod 8);
-  // FP64 accumulation in the fixed order k = warp, warp+8, …, then the 8 warps combined in order.
-  auto slice = [&]() {
+  // slot slice b of epoch e: lane ↔ slot, warp ↔ source CTA k ≡ warp (mod NW); each source word is
+  // re-read until it carries tag e.  FP64 accumulation in the fixed order k = warp, warp+NW, …,
+  // then the NW warps combined in order (deterministic).  Publishes b = −c/n tagged e and
+  // leaves S (Σ of the per-CTA row-sum partials, tagged e) in s_S.
+  auto slice = [&](unsigned e) {
     const int s0 = (int)((long)b * NS / G), s1 = (int)((long)(b + 1) * NS / G);
-    constexpr int WS = kResThreads / 32;
-    double sv[kResKMax];                                 // Spart loads issued first (overlap)
-    if (warp == 0) {
-#pragma unroll
-      for (int i = 0; i < kResKMax; ++i) sv[i] = (lane + 32 * i < G) ? __ldcg(P.Spart + lane + 32 * i) : 0.0;
-    }
+    constexpr int NI = (32 * kResKMax + NW - 1) / NW;
     for (int sb = s0; sb < s1; sb += 32) {
       const int s = sb + lane;
       double acc = 0.0;
       if (s < s1) {
-        float v[(32 * kResKMax + WS - 1) / WS];
+        unsigned w[NI];
 #pragma unroll
-        for (int i = 0; i < (32 * kResKMax + WS - 1) / WS; ++i) {
-          const int k = warp + i * WS;
-          v[i] = k < G ? __ldcg(P.colpart + (long)k * NS + s) : 0.f;
+        for (int i = 0; i < NI; ++i) {
+          const int k = warp + i * NW;
+          w[i] = k < G ? ld_w(P.colpart + (long)k * NS + s) : ptag(0.f, e);
         }
+        bool ok;
+        do {
+          ok = true;
 #pragma unroll
-        for (int i = 0; i < (32 * kResKMax + WS - 1) / WS; ++i) acc += (double)v[i];
+          for (int i = 0; i < NI; ++i)
+            if (!pok(w[i], e)) { ok = false; w[i] = ld_w(P.colpart + (long)(warp + i * NW) * NS + s); }
+        } while (!ok);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) acc += (double)pval(w[i]);
       }
       s_red2[warp][lane] = acc;
       __syncthreads();
       if (warp == 0 && s < s1) {
         double cs = 0.0;
 #pragma unroll
-        for (int w = 0; w < WS; ++w) cs += s_red2[w][lane];
-        const int f = s >> 2, e = s & 3, c = f >> 7, tt = f & 127;
-        const long colj = (long)tt * CPT + 4 * c + e;
-        __stcg(P.bvec + s, colj < n ? (float)(-cs / dn) : -CUDART_INF_F);
+        for (int w = 0; w < NW; ++w) cs += s_red2[w][lane];
+        const int f = s >> 2, e4 = s & 3, c = f >> 7, tt = f & 127;
+        const long colj = (long)tt * CPT + 4 * c + e4;
+        st_w(P.bvec + s, ptag(colj < n ? (float)(cs / dn) : CUDART_INF_F, e));   // |b_j| = c_j/n
       }
       __syncthreads();
     }
-    if (warp == 0) {
+    if (warp == 1) {                                     // S of epoch e (row-sum partials, parity buffer)
       double sacc = 0.0;
 #pragma unroll
-      for (int i = 0; i < kResKMax; ++i) sacc += sv[i];
+      for (int i = 0; i < kResKMax; ++i)
+        if (lane + 32 * i < G) sacc += wait_d1(P.Spart + (size_t)(e & 1) * G + lane + 32 * i, (e >> 1) & 1u);
       sacc = warp_sum_d(sacc);
       if (lane == 0) s_S = sacc;
     }
@@ -383,14 +475,14 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
 
   // ---------------- phase S: Y0 = s·X (on chip) and its sums ----------------
   sweep_scale();
-  gbar();
-  slice();
-  gbar();
+  unsigned ep = 1;                                       // epoch of the current exchange
+  slice(ep);
+  __syncthreads();
 
   // ---------------- pass loop (device-side stop decision, identical in every CTA) ----------------
   int j = 0;
   double gam = 0.0;
-  long long tacc[6] = {0, 0, 0, 0, 0, 0};   // dev timing (P.dbg): bload, sweep, barA, slice, barB
+  long long tacc[6] = {0, 0, 0, 0, 0, 0};   // dev timing (P.dbg): bload, sweep, -, slice, -
   auto now = [&]() -> long long {
     long long v = 0;
     if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -398,47 +490,61 @@ __global__ void __launch_bounds__(kResThreads, 1) sdsn_res_kernel(ResParams P) {
   };
   for (;; ++j) {
     long long t0 = now();
-    const double S = s_S;
+    const double S = s_S;                               // written by warp 1 in slice(ep), synced
     gam = S / dn - 1.0;                                                 // γ_j
     if (b == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[j] = gam;
     const bool last = P.sdsn_fixed > 0 ? (j + 1 >= P.sdsn_fixed)
                                        : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
     const double abase = 1.0 / dn + S / nn;
-    for (int i = tid; i < R; i += kResThreads) s_a[i] = (float)(abase - s_r[i] / dn);
-    float bv[CPT];
+    for (int i = tid; i < R; i += THREADS) s_a[i] = (float)(abase - s_r[i] / dn);
+    float2 bv[CH / 2];                                   // b_j pairs (register pairs for FADD2)
+    {
+      uint4 w[VH];
 #pragma unroll
-    for (int c = 0; c < V; ++c) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(P.bvec) + c * 128 + t);
-      bv[4 * c] = v.x; bv[4 * c + 1] = v.y; bv[4 * c + 2] = v.z; bv[4 * c + 3] = v.w;
+      for (int c = 0; c < VH; ++c) w[c] = ld_w4(P.bvec + (size_t)((c0 + c) * 128 + t) * 4);
+      bool ok;
+      do {                                               // wait for every b of epoch ep
+        ok = true;
+#pragma unroll
+        for (int c = 0; c < VH; ++c) {
+          if (!pok(w[c].x, ep) || !pok(w[c].y, ep) || !pok(w[c].z, ep) || !pok(w[c].w, ep)) {
+            ok = false;
+            w[c] = ld_w4(P.bvec + (size_t)((c0 + c) * 128 + t) * 4);
+          }
+        }
+      } while (!ok);
+#pragma unroll
+      for (int c = 0; c < VH; ++c) {                     // b = −|b|; −0 and −∞ (padding) as stored
+        bv[2 * c] = make_float2(-pval(w[c].x), -pval(w[c].y));
+        bv[2 * c + 1] = make_float2(-pval(w[c].z), -pval(w[c].w));
+      }
     }
     __syncthreads();
     long long t1 = now();
-    sweep_pass(bv);
+    sweep_pass(bv, last ? 0u : ep + 1);
     __syncthreads();
     long long t2 = now();
     if (last) break;
-    gbar();
-    long long t3 = now();
-    slice();
+    ++ep;
+    slice(ep);
     __syncthreads();
     long long t4 = now();
-    gbar();
-    long long t5 = now();
-    tacc[0] += t1 - t0; tacc[1] += t2 - t1; tacc[2] += t3 - t2; tacc[3] += t4 - t3; tacc[4] += t5 - t4;
+    tacc[0] += t1 - t0; tacc[1] += t2 - t1; tacc[3] += t4 - t2;
     tacc[5] += 1;
   }
   if (P.dbg && tid == 0) {
     for (int k = 0; k < 6; ++k) P.dbg[b * 8 + k] = tacc[k];
+    P.dbg[b * 8 + 2] = tfine[0]; P.dbg[b * 8 + 4] = tfine[1]; P.dbg[b * 8 + 6] = tfine[2]; P.dbg[b * 8 + 7] = tfine[3];
   }
 
   // ---------------- D = Y_final → global (row-major, ld) ----------------
   for (int r = g; r < R; r += 2) {
-    float x[CPT];
+    float x[CH];
     load_row(r, x);
     float* grow = P.Y + (r0 + r) * ld;
 #pragma unroll
-    for (int c = 0; c < V; ++c) {
-      const long col = (long)t * CPT + 4 * c;
+    for (int c = 0; c < VH; ++c) {
+      const long col = (long)t * CPT + 4 * (c0 + c);
       if (col + 3 < n) {
         *reinterpret_cast<float4*>(grow + col) = make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
       } else {
@@ -486,10 +592,17 @@ cudaError_t launch_res_t(ResParams p, cudaStream_t st, int G) {
   if (dsm < (size_t)kResMinSmem) dsm = kResMinSmem;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(p.flags, 0, sizeof(unsigned), st);
+  const size_t ns = RC<CPT>::NS;
+  p.Spart = p.xchg;                                      // [2][G] u64, tag bit 1 initially (0x80 bytes)
+  p.Mpart = p.Spart + 2 * (size_t)G;                     // [G] u64
+  p.colpart = reinterpret_cast<unsigned*>(p.xchg + ((3 * (size_t)G + 1) & ~(size_t)1));   // [G][NS] u32, 16-B aligned
+  p.bvec = p.colpart + (size_t)G * ns;                   // [NS] u32
+  e = cudaMemsetAsync(p.Spart, 0x80, 2 * (size_t)G * sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(p.Mpart, 0, (size_t)G * sizeof(uint64_t) + 8 + ((size_t)G * ns + ns) * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   void* args[] = {&p};
-  return cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(kResThreads), args, dsm, st);
+  return cudaLaunchCooperativeKernel((const void*)fn, dim3(G), dim3(RK<CPT>::THREADS), args, dsm, st);
 }
 
 }  // namespace
@@ -512,6 +625,11 @@ int sdsn_res_grid(long n, int num_sms) {
 }
 
 long sdsn_res_slots(long n) { return 128L * cpt_for(n); }
+
+size_t sdsn_res_xchg_words(long n, int num_sms) {         // in 8-byte words
+  const size_t ns = (size_t)sdsn_res_slots(n);
+  return 3 * (size_t)num_sms + 2 + ((size_t)num_sms * ns + ns + 1) / 2;
+}
 
 cudaError_t launch_sdsn_resident(const ResParams& p, cudaStream_t st, int num_sms) {
   const int G = sdsn_res_grid(p.n, num_sms);
