@@ -50,7 +50,7 @@ constexpr int kResKMax = 5;                  // G ≤ 32·kResKMax CTAs (148 SMs
 // dynamic shared memory: SMEM-resident rows, column staging, per-thread row partials, s_r, s_a
 size_t res_smem_bytes(int cpt, int rs, int R) {
   const size_t ns = 128 * (size_t)cpt;
-  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 8 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
+  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 64 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
 }
 
 __device__ __forceinline__ uint64_t tag_f(float v, unsigned e) {
@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   const int Rmax = P.rmax;
   float4* s_rows = reinterpret_cast<float4*>(dsm);                    // [RS][V·128] slot layout
   float4* s_col = s_rows + (size_t)RS * V * 128;                      // [V·128] column staging
-  float* s_rowpart = reinterpret_cast<float*>(s_col + V * 128);       // [Rmax][8] per-warp row partials
-  double* s_r = reinterpret_cast<double*>(s_rowpart + Rmax * 8);     // [Rmax] row sums (FP64)
+  float* s_rowpart = reinterpret_cast<float*>(s_col + V * 128);       // [Rmax][8 warps][8 lanes] row partials
+  double* s_r = reinterpret_cast<double*>(s_rowpart + Rmax * 64);    // [Rmax] row sums (FP64)
   float* s_a = reinterpret_cast<float*>(s_r + Rmax);                 // [Rmax] a_i (FP32)
   __shared__ uint32_t s_tmem;
   __shared__ double s_red[NW];
@@ -309,13 +309,17 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       }
     }
     const long long e1a = gt();
-    // row sums: the 4·NH per-warp partials of each row, combined in FP64 in a fixed order
-    for (int i = tid; i < R; i += THREADS) {
-      const float* pp = s_rowpart + i * 8;
+    // row sums: the 8·4·NH partials of each row (8 lanes of each contributing warp), combined in
+    // FP64 in a fixed order: one warp per row, lanes take (warp slot, lane) pairs, then a warp tree
+    for (int i = warp; i < R; i += NW) {
+      const float* pp = s_rowpart + i * 64;
       double acc = 0.0;
+      if (lane < 4 * K::NH) {
 #pragma unroll
-      for (int k = 0; k < 4 * K::NH; ++k) acc += (double)pp[k];
-      s_r[i] = acc;
+        for (int k = 0; k < 8; ++k) acc += (double)pp[lane * 8 + k];
+      }
+      acc = warp_sum_d(acc);
+      if (lane == 0) s_r[i] = acc;
     }
     const long long e1b = gt();
     __syncthreads();
@@ -329,17 +333,17 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     const long long e2 = gt();
     tfine[1] += e1a - e1; tfine[2] += e1b - e1a; tfine[3] += e1c - e1b; tfine[0] += e2 - e1c;
   };
-  // this warp's partials of rows ra and rb (rb < 0: none): two interleaved shuffle trees, lane 0
-  // stores them at slot 4·h + q of the row (fixed order, deterministic)
+  // this warp's partials of rows ra and rb (rb < 0: none): two shuffle levels (32 → 8 lanes), then
+  // lanes 0-7 store at [row][4·h + q][lane] (fixed positions, deterministic)
   auto put_rowparts = [&](int ra, float va, int rb, float vb) {
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = 16; o >= 8; o >>= 1) {
       va += __shfl_xor_sync(0xffffffffu, va, o);
       vb += __shfl_xor_sync(0xffffffffu, vb, o);
     }
-    if (lane == 0) {
-      s_rowpart[ra * 8 + 4 * h + q] = va;
-      if (rb >= 0) s_rowpart[rb * 8 + 4 * h + q] = vb;
+    if (lane < 8) {
+      s_rowpart[ra * 64 + (4 * h + q) * 8 + lane] = va;
+      if (rb >= 0) s_rowpart[rb * 64 + (4 * h + q) * 8 + lane] = vb;
     }
   };
 
@@ -387,11 +391,17 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     float2 col2[CH / 2];
 #pragma unroll
     for (int k = 0; k < CH / 2; ++k) col2[k] = make_float2(0.f, 0.f);
-    int ra = g;
-    const int Rl = (P.dbgmode & 1) ? min(R, RT) : R;    // dev timing knobs (FRAM_RES_DBGMODE)
-    if (P.dbgmode & 2) ra = g + ((RT - g + 3) / 4) * 4;
-    for (; ra + 2 < Rl; ra += 4) {                       // rows g, g+2, … two at a time
-      const int rb = ra + 2;
+    // rows of this row group: with rows in both TMEM and shared memory, group 0 takes the TMEM rows
+    // and group 1 the shared-memory rows so the two datapaths work concurrently; otherwise rows
+    // alternate between the groups
+    int rbeg, rend, rstep;
+    if (R > RT) { rbeg = g == 0 ? 0 : RT; rend = g == 0 ? RT : R; rstep = 1; }
+    else { rbeg = g; rend = R; rstep = 2; }
+    if (P.dbgmode & 1) rend = min(rend, RT);           // dev timing knobs (FRAM_RES_DBGMODE)
+    if ((P.dbgmode & 2) && rbeg < RT) rbeg = rend;
+    int ra = rbeg;
+    for (; ra + rstep < rend; ra += 2 * rstep) {         // two rows at a time
+      const int rb = ra + rstep;
       float xa[CH], xb[CH];
       if (rb < RT) {                                     // both rows in TMEM: one wait for two loads
         uint32_t va[CH], vb[CH];
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       store_row(rb, xb);
       put_rowparts(ra, sa, rb, sb);
     }
-    if (ra < Rl) {
+    if (ra < rend) {
       float xa[CH];
       load_row(ra, xa);
       const float sa = pass_rows(xa, s_a[ra], bv, col2);
@@ -431,6 +441,13 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   auto slice = [&](unsigned e) {
     const int s0 = (int)((long)b * NS / G), s1 = (int)((long)(b + 1) * NS / G);
     constexpr int NI = (32 * kResKMax + NW - 1) / NW;
+    uint64_t spw[kResKMax];                              // S partials: loads issued first (overlap)
+    const unsigned sbit = (e >> 1) & 1u;
+    const uint64_t* sp = P.Spart + (size_t)(e & 1) * G;
+    if (warp == 1) {
+#pragma unroll
+      for (int i = 0; i < kResKMax; ++i) spw[i] = (lane + 32 * i < G) ? ld_tag(sp + lane + 32 * i) : 0ull;
+    }
     for (int sb = s0; sb < s1; sb += 32) {
       const int s = sb + lane;
       double acc = 0.0;
@@ -466,8 +483,12 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     if (warp == 1) {                                     // S of epoch e (row-sum partials, parity buffer)
       double sacc = 0.0;
 #pragma unroll
-      for (int i = 0; i < kResKMax; ++i)
-        if (lane + 32 * i < G) sacc += wait_d1(P.Spart + (size_t)(e & 1) * G + lane + 32 * i, (e >> 1) & 1u);
+      for (int i = 0; i < kResKMax; ++i) {
+        if (lane + 32 * i < G) {
+          while ((unsigned)(spw[i] >> 63) != sbit) spw[i] = ld_tag(sp + lane + 32 * i);
+          sacc += __longlong_as_double((long long)(spw[i] & 0x7fffffffffffffffull));
+        }
+      }
       sacc = warp_sum_d(sacc);
       if (lane == 0) s_S = sacc;
     }
@@ -593,11 +614,15 @@ cudaError_t launch_res_t(ResParams p, cudaStream_t st, int G) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   if (e != cudaSuccess) return e;
   const size_t ns = RC<CPT>::NS;
-  p.Spart = p.xchg;                                      // [2][G] u64, tag bit 1 initially (0x80 bytes)
+  p.Spart = p.xchg;                                      // [2][G] u64; tag of epoch e is bit (e>>1)&1 in
+                                                         // buffer e&1: first used at e=2 (buf 0, tag 1)
+                                                         // and e=1 (buf 1, tag 0) → init tags 0 and 1
   p.Mpart = p.Spart + 2 * (size_t)G;                     // [G] u64
   p.colpart = reinterpret_cast<unsigned*>(p.xchg + ((3 * (size_t)G + 1) & ~(size_t)1));   // [G][NS] u32, 16-B aligned
   p.bvec = p.colpart + (size_t)G * ns;                   // [NS] u32
-  e = cudaMemsetAsync(p.Spart, 0x80, 2 * (size_t)G * sizeof(uint64_t), st);
+  e = cudaMemsetAsync(p.Spart, 0, (size_t)G * sizeof(uint64_t), st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(p.Spart + G, 0x80, (size_t)G * sizeof(uint64_t), st);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(p.Mpart, 0, (size_t)G * sizeof(uint64_t) + 8 + ((size_t)G * ns + ns) * sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
