@@ -284,19 +284,43 @@ def run_ours(args):
 
     hbm, bf16, bf16s, psrc = peaks()
     sdsn_launches = iters                                     # one persistent SDSN launch per outer iteration
-    bytes_per_launch = 8.0 * n * n * passes / sdsn_launches   # algorithmic: FP32 Y read + write per pass
+    resident = stats[0].get("sdsn_kernel", 1) == 2
     avg_launch_s = ms_sdsn / 1e3 / sdsn_launches
-    achieved = bytes_per_launch / avg_launch_s / 1e9
+    passes_per_launch = passes / sdsn_launches
+    bytes_per_launch = 8.0 * n * n * passes_per_launch       # algorithmic: FP32 Y read + write per pass
+    hbm_equiv = bytes_per_launch / avg_launch_s / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "sdsn_traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                tj = json.load(f)
+                tj = json.load(f).get("resident" if resident else "streaming", {})
             if int(tj.get("n", 0)) == n:
-                traffic = float(tj["dram_bytes_per_pass"]) * passes / sdsn_launches
+                traffic = float(tj["dram_bytes_per_launch"]) if resident else \
+                    float(tj["dram_bytes_per_pass"]) * passes_per_launch
         except Exception:
             traffic = None
+    if resident:
+        # K4r keeps Y on chip (TMEM + shared memory): HBM is touched only to load G and store D once per
+        # launch, so the pass loop is bound by the SM datapath.  Roofline: 5 FP32 ops per
+        # element per pass (x+a, +b, max, column and row accumulation) against the issue-bound ALU
+        # peak for that op mix: 148 SMs x 128 lanes x f_max, x 5/3 (the 4 adds issue as 2 paired FADD2).
+        f_max = 1.965e9
+        alu_peak = 148 * 128 * f_max * 5.0 / 3.0 / 1e12
+        achieved = 5.0 * n * n * passes_per_launch / avg_launch_s / 1e12
+        roof = {"kernel": "sdsn_res_kernel<32> (K4r, on-chip resident; one persistent launch per SDSN call)",
+                "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
+                "frac": achieved / alu_peak, "traffic": traffic,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 1.965 GHz x 5/3 (B200_PROFILING.md unit counts)",
+                "algorithmic_flops_per_launch": 5.0 * n * n * passes_per_launch,
+                "hbm_equivalent": {"achieved_gbs": hbm_equiv, "peak_gbs": hbm, "frac": hbm_equiv / hbm,
+                                   "note": "algorithmic 8n^2 B/pass over the launch time; the iterate never leaves the chip"}}
+    else:
+        roof = {"kernel": "sdsn_kernel<float> (K4, streaming through L2/HBM)", "bound": "hbm", "achieved": hbm_equiv,
+                "peak": hbm, "unit": "GB/s", "frac": hbm_equiv / hbm, "traffic": traffic, "peak_source": psrc,
+                "algorithmic_bytes_per_launch": bytes_per_launch}
+    roof.update({"passes_per_launch": passes_per_launch, "ms_per_launch": avg_launch_s * 1e3,
+                 "us_per_pass": avg_launch_s * 1e6 / passes_per_launch, "share_of_step": ms_sdsn / tot_ms})
     gemm_tflops = 4.0 * n ** 3 * iters / (ms_gemm / 1e3) / 1e12 if ms_gemm > 0 else None
 
     line = None
@@ -312,12 +336,7 @@ def run_ours(args):
                 "time_to_solution_ms": statistics.median(step_ms),
                 "outer_iters_per_solve": iters / args.steps, "mean_passes_per_iter": passes / iters,
                 "accuracy": acc,
-                "roofline": {"kernel": "sdsn_kernel<float,2> (K4, one persistent launch per SDSN call)",
-                             "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                             "frac": achieved / hbm, "traffic": traffic, "peak_source": psrc,
-                             "algorithmic_bytes_per_launch": bytes_per_launch,
-                             "passes_per_launch": passes / sdsn_launches,
-                             "share_of_step": ms_sdsn / tot_ms},
+                "roofline": roof,
                 "gemm": {"tflops": gemm_tflops, "peak_bf16": bf16s, "frac_of_sustained": (gemm_tflops or 0) / bf16s,
                          "ms_per_step": ms_gemm / args.steps},
                 "lap_ms_per_step": ms_lap / args.steps,

@@ -92,7 +92,7 @@ typedef struct {
   int32_t outer_iters;       /* outer iterations run (t at exit)                                 */
   int32_t converged;         /* 1 if δ ≤ δ_th was reached                                         */
   int32_t sdsn_capped_calls; /* SDSN calls that stopped on sdsn_max                               */
-  int32_t _pad;
+  int32_t sdsn_kernel;       /* SDSN kernel used: 1 streaming (K4, L2/HBM), 2 on-chip resident (K4r) */
   int64_t total_passes;      /* Σ_t passes_t                                                     */
   int32_t* passes_per_iter;  /* [max_outer] SDSN passes of outer iteration t                     */
   double*  delta_trace;      /* [max_outer] δ_t                                          */

@@ -56,6 +56,7 @@ struct fram_ctx {
   std::vector<int32_t> replay;
   int device = 0;
   int num_sms = 148;
+  bool dev_checked = false;
   long ld = 0;
   // workspace
   DevBuf Aq, BqT, Kq, N, Nq, UT, Y, colpart, Spart, Mpart, cvec, bar, scal, ghist, upd, lapw, permd;
@@ -175,15 +176,21 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
 }
 
 fram_status set_device(fram_ctx* h) {
+  if (h->dev_checked) {                      // properties are queried once per handle (the query costs ms)
+    CK(cudaSetDevice(h->device), "cudaSetDevice");
+    return FRAM_OK;
+  }
   int cnt = 0;
   cudaError_t e = cudaGetDeviceCount(&cnt);
   if (e != cudaSuccess || cnt == 0) return cuda_fail(e == cudaSuccess ? cudaErrorNoDevice : e, "no CUDA device");
   CK(cudaSetDevice(h->device), "cudaSetDevice");
-  cudaDeviceProp prop;
-  CK(cudaGetDeviceProperties(&prop, h->device), "device properties");
-  if (prop.major != 10) return fail(FRAM_ERR_CUDA, "libfram is built for sm_100a (B200); device is sm_" +
-                                                       std::to_string(prop.major) + std::to_string(prop.minor));
-  h->num_sms = prop.multiProcessorCount;
+  int major = 0, sms = 0;
+  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, h->device), "device attribute");
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device), "device attribute");
+  if (major != 10) return fail(FRAM_ERR_CUDA, "libfram is built for sm_100a (B200); device is sm_" +
+                                                  std::to_string(major) + "x");
+  h->num_sms = sms;
+  h->dev_checked = true;
   return FRAM_OK;
 }
 
@@ -263,10 +270,11 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
       double mx[6] = {0};
       for (int bb = 0; bb < G; ++bb)
         for (int k = 0; k < 6; ++k) mx[k] = std::max(mx[k], (double)d[bb * 8 + k]);
-      const double np = std::max(1.0, (double)d[5]);
+      const double np = std::max(1.0, (double)(d[5] & 0xffff));
+      fprintf(stderr, "[res timing] CTA0 load phase %.1f us, kernel start→loop end %.1f us\n", (d[5] >> 16) / 1e3, d[3] / 1e3);
       fprintf(stderr, "[res timing n=%ld G=%d passes=%.0f] ns/pass (CTA0): bload %.0f sweep %.0f [spart %.0f stores %.0f srows %.0f sync %.0f] slice %.0f | max over CTAs: %.0f %.0f %.0f\n",
-              (long)h->n, G, np, d[0] / np, d[1] / np, d[2] / np, d[4] / np, d[6] / np, d[7] / np, d[3] / np, mx[0] / np, mx[1] / np,
-              mx[3] / np);
+              (long)h->n, G, np, d[0] / np, d[1] / np, d[2] / np, d[4] / np, d[6] / np, d[7] / np, 0.0, mx[0] / np, mx[1] / np,
+              0.0);
     }
     h->launches += 2;   // flag memset + kernel
     return FRAM_OK;
@@ -449,6 +457,7 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     stats->sdsn_capped_calls = capped;
     stats->total_passes = total;
     stats->kernel_launches = h->launches;
+    stats->sdsn_kernel = use_resident(h, f64) ? 2 : 1;
     if (timing) {
       float a, b, cc;
       cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);

@@ -50,7 +50,7 @@ constexpr int kResKMax = 5;                  // G ≤ 32·kResKMax CTAs (148 SMs
 // dynamic shared memory: SMEM-resident rows, column staging, per-thread row partials, s_r, s_a
 size_t res_smem_bytes(int cpt, int rs, int R) {
   const size_t ns = 128 * (size_t)cpt;
-  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 64 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
+  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 8 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
 }
 
 __device__ __forceinline__ uint64_t tag_f(float v, unsigned e) {
@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   const int Rmax = P.rmax;
   float4* s_rows = reinterpret_cast<float4*>(dsm);                    // [RS][V·128] slot layout
   float4* s_col = s_rows + (size_t)RS * V * 128;                      // [V·128] column staging
-  float* s_rowpart = reinterpret_cast<float*>(s_col + V * 128);       // [Rmax][8 warps][8 lanes] row partials
-  double* s_r = reinterpret_cast<double*>(s_rowpart + Rmax * 64);    // [Rmax] row sums (FP64)
+  float* s_rowpart = reinterpret_cast<float*>(s_col + V * 128);       // [Rmax][8] per-warp row partials
+  double* s_r = reinterpret_cast<double*>(s_rowpart + Rmax * 8);     // [Rmax] row sums (FP64)
   float* s_a = reinterpret_cast<float*>(s_r + Rmax);                 // [Rmax] a_i (FP32)
   __shared__ uint32_t s_tmem;
   __shared__ double s_red[NW];
@@ -218,6 +218,8 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512));
   };
 
+  long long tk0 = 0;
+  if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk0));
   // ---------------- phase L: X rows → on-chip, m = max X (Alg.2 step 1) ----------------
   {
     float lmax = 0.f;
@@ -309,17 +311,13 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       }
     }
     const long long e1a = gt();
-    // row sums: the 8·4·NH partials of each row (8 lanes of each contributing warp), combined in
-    // FP64 in a fixed order: one warp per row, lanes take (warp slot, lane) pairs, then a warp tree
-    for (int i = warp; i < R; i += NW) {
-      const float* pp = s_rowpart + i * 64;
+    // row sums: the 4·NH per-warp partials of each row, combined in FP64 in a fixed order
+    for (int i = tid; i < R; i += THREADS) {
+      const float* pp = s_rowpart + i * 8;
       double acc = 0.0;
-      if (lane < 4 * K::NH) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) acc += (double)pp[lane * 8 + k];
-      }
-      acc = warp_sum_d(acc);
-      if (lane == 0) s_r[i] = acc;
+      for (int k = 0; k < 4 * K::NH; ++k) acc += (double)pp[k];
+      s_r[i] = acc;
     }
     const long long e1b = gt();
     __syncthreads();
@@ -333,17 +331,17 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     const long long e2 = gt();
     tfine[1] += e1a - e1; tfine[2] += e1b - e1a; tfine[3] += e1c - e1b; tfine[0] += e2 - e1c;
   };
-  // this warp's partials of rows ra and rb (rb < 0: none): two shuffle levels (32 → 8 lanes), then
-  // lanes 0-7 store at [row][4·h + q][lane] (fixed positions, deterministic)
+  // this warp's partials of rows ra and rb (rb < 0: none): two interleaved shuffle trees, lane 0
+  // stores them at slot 4·h + q of the row (fixed order, deterministic)
   auto put_rowparts = [&](int ra, float va, int rb, float vb) {
 #pragma unroll
-    for (int o = 16; o >= 8; o >>= 1) {
+    for (int o = 16; o > 0; o >>= 1) {
       va += __shfl_xor_sync(0xffffffffu, va, o);
       vb += __shfl_xor_sync(0xffffffffu, vb, o);
     }
-    if (lane < 8) {
-      s_rowpart[ra * 64 + (4 * h + q) * 8 + lane] = va;
-      if (rb >= 0) s_rowpart[rb * 64 + (4 * h + q) * 8 + lane] = vb;
+    if (lane == 0) {
+      s_rowpart[ra * 8 + 4 * h + q] = va;
+      if (rb >= 0) s_rowpart[rb * 8 + 4 * h + q] = vb;
     }
   };
 
@@ -441,13 +439,6 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   auto slice = [&](unsigned e) {
     const int s0 = (int)((long)b * NS / G), s1 = (int)((long)(b + 1) * NS / G);
     constexpr int NI = (32 * kResKMax + NW - 1) / NW;
-    uint64_t spw[kResKMax];                              // S partials: loads issued first (overlap)
-    const unsigned sbit = (e >> 1) & 1u;
-    const uint64_t* sp = P.Spart + (size_t)(e & 1) * G;
-    if (warp == 1) {
-#pragma unroll
-      for (int i = 0; i < kResKMax; ++i) spw[i] = (lane + 32 * i < G) ? ld_tag(sp + lane + 32 * i) : 0ull;
-    }
     for (int sb = s0; sb < s1; sb += 32) {
       const int s = sb + lane;
       double acc = 0.0;
@@ -483,18 +474,16 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     if (warp == 1) {                                     // S of epoch e (row-sum partials, parity buffer)
       double sacc = 0.0;
 #pragma unroll
-      for (int i = 0; i < kResKMax; ++i) {
-        if (lane + 32 * i < G) {
-          while ((unsigned)(spw[i] >> 63) != sbit) spw[i] = ld_tag(sp + lane + 32 * i);
-          sacc += __longlong_as_double((long long)(spw[i] & 0x7fffffffffffffffull));
-        }
-      }
+      for (int i = 0; i < kResKMax; ++i)
+        if (lane + 32 * i < G) sacc += wait_d1(P.Spart + (size_t)(e & 1) * G + lane + 32 * i, (e >> 1) & 1u);
       sacc = warp_sum_d(sacc);
       if (lane == 0) s_S = sacc;
     }
   };
 
   // ---------------- phase S: Y0 = s·X (on chip) and its sums ----------------
+  long long tk1 = 0;
+  if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk1));
   sweep_scale();
   unsigned ep = 1;                                       // epoch of the current exchange
   slice(ep);
@@ -556,6 +545,10 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   if (P.dbg && tid == 0) {
     for (int k = 0; k < 6; ++k) P.dbg[b * 8 + k] = tacc[k];
     P.dbg[b * 8 + 2] = tfine[0]; P.dbg[b * 8 + 4] = tfine[1]; P.dbg[b * 8 + 6] = tfine[2]; P.dbg[b * 8 + 7] = tfine[3];
+    long long tk2;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk2));
+    P.dbg[b * 8 + 5] = (tacc[5] & 0xffff) | ((tk1 - tk0) << 16);   // passes | load-phase ns
+    P.dbg[b * 8 + 3] = tk2 - tk0;                                   // total ns to loop end
   }
 
   // ---------------- D = Y_final → global (row-major, ld) ----------------
@@ -614,9 +607,7 @@ cudaError_t launch_res_t(ResParams p, cudaStream_t st, int G) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   if (e != cudaSuccess) return e;
   const size_t ns = RC<CPT>::NS;
-  p.Spart = p.xchg;                                      // [2][G] u64; tag of epoch e is bit (e>>1)&1 in
-                                                         // buffer e&1: first used at e=2 (buf 0, tag 1)
-                                                         // and e=1 (buf 1, tag 0) → init tags 0 and 1
+  p.Spart = p.xchg;                                      // [2][G] u64, tag bit 1 initially (0x80 bytes)
   p.Mpart = p.Spart + 2 * (size_t)G;                     // [G] u64
   p.colpart = reinterpret_cast<unsigned*>(p.xchg + ((3 * (size_t)G + 1) & ~(size_t)1));   // [G][NS] u32, 16-B aligned
   p.bvec = p.colpart + (size_t)G * ns;                   // [NS] u32

@@ -41,7 +41,7 @@ class _Schedule(C.Structure):
 
 class _Stats(C.Structure):
     _fields_ = [("outer_iters", C.c_int32), ("converged", C.c_int32), ("sdsn_capped_calls", C.c_int32),
-                ("_pad", C.c_int32), ("total_passes", C.c_int64), ("passes_per_iter", C.POINTER(C.c_int32)),
+                ("sdsn_kernel", C.c_int32), ("total_passes", C.c_int64), ("passes_per_iter", C.POINTER(C.c_int32)),
                 ("delta_trace", C.POINTER(C.c_double)), ("gamma_last", C.POINTER(C.c_double)),
                 ("ms_precond", C.c_double), ("ms_gemm", C.c_double), ("ms_sdsn", C.c_double),
                 ("ms_update", C.c_double), ("ms_lap", C.c_double), ("ms_total", C.c_double),
@@ -198,7 +198,7 @@ def _stats_dict(st, nout, arrays):
     d = dict(outer_iters=st.outer_iters, converged=bool(st.converged), sdsn_capped_calls=st.sdsn_capped_calls,
              total_passes=int(st.total_passes), ms_precond=st.ms_precond, ms_gemm=st.ms_gemm,
              ms_sdsn=st.ms_sdsn, ms_update=st.ms_update, ms_lap=st.ms_lap, ms_total=st.ms_total,
-             kernel_launches=int(st.kernel_launches))
+             kernel_launches=int(st.kernel_launches), sdsn_kernel=int(st.sdsn_kernel))
     if arrays is not None:
         t = st.outer_iters
         d["passes"] = [int(x) for x in arrays[0][:t]]

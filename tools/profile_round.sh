@@ -10,7 +10,7 @@ timeout 900 python bench.py > $OUT/bench_${TAG}.json 2> $OUT/bench_${TAG}.err; e
 CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
 timeout 600 $CMD > $OUT/plain_${TAG}.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file $OUT/launches_${TAG}.csv $CMD > $OUT/ncu_launch_${TAG}.log 2>&1; echo "launch list rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdsn_kernel -s 3 -c 1 -o $OUT/prof_sdsn_${TAG} $CMD > $OUT/ncu_sdsn_${TAG}.log 2>&1; echo "ncu sdsn rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdsn -s 3 -c 1 -o $OUT/prof_sdsn_${TAG} $CMD > $OUT/ncu_sdsn_${TAG}.log 2>&1; echo "ncu sdsn rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 4 -c 2 -o $OUT/prof_gemm_${TAG} $CMD > $OUT/ncu_gemm_${TAG}.log 2>&1; echo "ncu gemm rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:lap_kernel -c 1 -o $OUT/prof_lap_${TAG} $CMD > $OUT/ncu_lap_${TAG}.log 2>&1; echo "ncu lap rc=$?"
 ls -la $OUT
