@@ -92,7 +92,8 @@ typedef struct {
   int32_t outer_iters;       /* outer iterations run (t at exit)                                 */
   int32_t converged;         /* 1 if δ ≤ δ_th was reached                                         */
   int32_t sdsn_capped_calls; /* SDSN calls that stopped on sdsn_max                               */
-  int32_t sdsn_kernel;       /* SDSN kernel used: 1 streaming (K4, L2/HBM), 2 on-chip resident (K4r) */
+  int32_t sdsn_kernel;       /* SDSN kernel used: 1 streaming (K4), 2 on-chip resident (K4r),
+                                3 row-sharded per-pass kernels + NCCL (K4s)                          */
   int64_t total_passes;      /* Σ_t passes_t                                                     */
   int32_t* passes_per_iter;  /* [max_outer] SDSN passes of outer iteration t                     */
   double*  delta_trace;      /* [max_outer] δ_t                                          */
@@ -142,7 +143,14 @@ FRAM_API const char* fram_last_error(void);
  * The library owns an ncclComm; Python broadcasts the 128-byte id through torch.distributed.
  * In a sharded handle fram_solve's A, K, X0, X_out are the local row block
  * [rank·n/W, (rank+1)·n/W) (n % W == 0, row-major n/W × n); B (Ã) is full on every rank;
- * perm_out is full on every rank.  NCCL is loaded at run time (dlopen of libnccl.so.2). */
+ * perm_out is full on every rank.  NCCL is loaded at run time (dlopen of libnccl.so.2).
+ * Per outer iteration (Alg.1 steps 5-8): U_rᵀ = (N_r·Ã')ᵀ locally, all-gather of the U_rᵀ blocks
+ * (n²·esz bytes in total), G_r = A'_r·U + λK'_r, SDSN on the row block with one all-reduce of the
+ * n column sums and the mass per pass (FP64, n+1 values), the local update, and an all-reduce of
+ * (ΣΔ², ΣN²) for δ.  After the loop every rank all-gathers N and runs the same LAP (step 10).
+ * Mixed modes need (n/W) % 64 == 0.  The symmetry check (FRAM_FLAG_CHECK_SYMMETRY) covers Ã only
+ * (a row block of A cannot see its transpose).  fram_sdsn / fram_gradient / fram_lap /
+ * fram_solve_batched return FRAM_ERR_USAGE on a sharded handle. */
 FRAM_API fram_status fram_get_unique_id(uint8_t id[128]);
 FRAM_API fram_status fram_create_sharded(int64_t n, double lambda, const fram_schedule* s,
                                 const uint8_t id[128], int rank, int world, int device,

@@ -60,7 +60,8 @@ struct fram_ctx {
   long ld = 0;
   // workspace
   DevBuf Aq, BqT, Kq, N, Nq, UT, Y, colpart, Spart, Mpart, cvec, bar, scal, ghist, upd, lapw, permd;
-  DevBuf rcolpart, rbvec, rflags, rdbg;   // on-chip-resident SDSN (K4r)
+  DevBuf rcolpart, rbvec, rflags, rdbg;
+  DevBuf shUT, shUblk, shRsum, shSend, shRecv, shState, shNfull, shColpart, shScan;   // sharded solve   // on-chip-resident SDSN (K4r)
   DevBuf stA, stB, stK, stX0, stX;
   DevBuf scan;
   double* hscal = nullptr;          // pinned readback
@@ -307,8 +308,203 @@ fram_status common_checks(fram_ctx* h, int dt, fram_precision p) {
   if (!h) return fail(FRAM_ERR_USAGE, "null handle");
   if (dt < 0 || dt > 2) return fail(FRAM_ERR_USAGE, "bad dtype");
   if ((int)p < 0 || (int)p > 3) return fail(FRAM_ERR_USAGE, "bad precision");
-  if (h->shard) return fail(FRAM_ERR_USAGE, "use the sharded entry points for a sharded handle");
   return set_device(h);
+}
+
+// ---- row-sharded solve (config C5) ---------------------------------------------
+// Rank r owns rows I_r = [r·m, (r+1)·m), m = n/W, of A, K, N and G; Ã is replicated.  Per outer
+// iteration: GEMM1 U_rᵀ = (N_q,r·Ã')ᵀ (local) → all-gather of the U_rᵀ blocks → GEMM2
+// G_r = A'_r·U + λK'_r (K-blocked operand) → SDSN on the row block (per-pass kernels, all-reduce of
+// [column sums, mass]) → local update → all-reduce of (ΣΔ², ΣN²) → δ.  Finally N is all-gathered
+// and every rank runs the same deterministic LAP (identical perm everywhere).
+fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, const void* K, const double* X0,
+                          int op, cudaStream_t st, double* X_out, int32_t* perm_out, fram_stats* stats) {
+  fram::ShardCtx* sh = h->shard;
+  const int W = fram::shard_world(sh);
+  const long n = h->n, m = n / W, ld = h->ld;
+  const bool f64 = (op == 0);
+  const size_t es = op_size(op), ts = f64 ? 8 : 4;
+  std::string err;
+  auto nck = [&](fram_status s) -> fram_status { if (s != FRAM_OK) g_err = err; return s; };
+  if (!f64 && (m % 64 != 0)) return fail(FRAM_ERR_USAGE, "sharded mixed-precision solve needs (n/W) % 64 == 0");
+  h->launches = 0;
+  const bool timing = (h->sched.flags & FRAM_FLAG_TIME_PHASES) != 0;
+  // workspace (local rows m, full Ã)
+  CK(h->Aq.ensure((size_t)m * ld * es), "alloc A'");
+  CK(h->BqT.ensure((size_t)n * ld * es), "alloc B'");
+  if (K) CK(h->Kq.ensure((size_t)m * ld * ts), "alloc K'");
+  CK(h->N.ensure((size_t)m * ld * 8), "alloc N");
+  if (!f64) CK(h->Nq.ensure((size_t)m * ld * es), "alloc Nq");
+  CK(h->shUT.ensure((size_t)n * m * es), "alloc U");
+  CK(h->shUblk.ensure((size_t)n * n * es), "alloc U blocks");
+  CK(h->Y.ensure((size_t)m * ld * ts), "alloc G/Y");
+  const int G = fram::sdsn_sh_grid(m, h->num_sms, f64);
+  CK(h->shColpart.ensure((size_t)G * ld * ts), "alloc colpart");
+  CK(h->shRsum.ensure((size_t)m * 8), "alloc rsum");
+  CK(h->shSend.ensure((size_t)(ld + 8) * 8), "alloc send");
+  CK(h->shRecv.ensure((size_t)(ld + 8) * 8), "alloc recv");
+  CK(h->shState.ensure(sizeof(fram::ShardSdsnState)), "alloc state");
+  CK(h->ghist.ensure((size_t)sdsn_cap(h) * 8), "alloc ghist");
+  CK(h->upd.ensure((size_t)(h->num_sms * 4 * 2 + 16) * 8), "alloc upd");
+  CK(h->scal.ensure(kScalDoubles * 8), "alloc scal");
+  CK(h->shNfull.ensure((size_t)n * ld * 8), "alloc N full");
+  CK(h->lapw.ensure(fram::lap_work_bytes(n)), "alloc lap");
+  CK(h->permd.ensure((size_t)n * 4), "alloc perm");
+  CK(h->scan.ensure(sizeof(fram::PrecondScan)), "alloc scan");
+  CK(h->shScan.ensure(sizeof(fram::PrecondScan)), "alloc scan (reduced)");
+  if (!h->hscal) CK(cudaMallocHost((void**)&h->hscal, kScalDoubles * 8), "alloc pinned");
+  for (auto& e : h->ev)
+    if (!e) CK(cudaEventCreate(&e), "event create");
+  if (timing) CK(cudaEventRecord(h->ev[0], st), "event");
+  // stage inputs
+  fram_status rs;
+  const void *dA, *dB, *dK, *dX0;
+  if ((rs = stage_in(h, h->stA, A, (size_t)m * n * dt_size(dt), st, &dA)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stB, B, (size_t)n * n * dt_size(dt), st, &dB)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stK, K, (size_t)m * n * dt_size(dt), st, &dK)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stX0, X0, (size_t)m * n * 8, st, &dX0)) != FRAM_OK) return rs;
+  // K1: global c = max(A, Ã, K) and validation, all-reduced (max) over ranks
+  fram::PrecondScan* sc = h->scan.as<fram::PrecondScan>();
+  fram::PrecondScan* scr = h->shScan.as<fram::PrecondScan>();
+  const bool sym = (h->sched.flags & FRAM_FLAG_CHECK_SYMMETRY) != 0;
+  CK(fram::launch_precond_scan(nullptr, dB, nullptr, dt, n, sym, sc, nullptr, nullptr, st), "precond scan");
+  CK(fram::launch_precond_scan_rows(dA, dK, dt, m, n, sc, st), "precond scan rows");
+  h->launches += 2;
+  if (nck(fram::shard_allreduce_f64(sh, sc->maxv, scr->maxv, 3, true, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
+  if (nck(fram::shard_allreduce_u64_max(sh, reinterpret_cast<const uint64_t*>(&sc->bad_nonfinite),
+                                        reinterpret_cast<uint64_t*>(&scr->bad_nonfinite), 3, st, &err)) != FRAM_OK)
+    return FRAM_ERR_NCCL;
+  fram::PrecondScan hs;
+  CK(cudaMemcpyAsync(&hs, scr, sizeof(hs), cudaMemcpyDeviceToHost, st), "scan readback");
+  CK(cudaStreamSynchronize(st), "scan sync");
+  if (hs.bad_nonfinite) return fail(FRAM_ERR_DATA, "non-finite entries in A, B or K");
+  if (hs.bad_negative) return fail(FRAM_ERR_DATA, "negative entries in A, B or K (P:55)");
+  if (hs.bad_asym) return fail(FRAM_ERR_DATA, "B is not symmetric (P:55, R28)");
+  if (!(std::max(std::max(hs.maxv[0], hs.maxv[1]), hs.maxv[2]) > 0)) return fail(FRAM_ERR_DATA, "c = max(A, B, K) = 0 (S:344)");
+  CK(fram::launch_precond_apply(dA, dB, dK, dt, n, ld, scr->maxv, op, h->Aq.p, h->BqT.p, dK ? h->Kq.p : nullptr,
+                                f64, st, m),
+     "precond apply");
+  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dX0, m, n, ld, st), "init N");
+  h->launches += 2;
+  if (timing) CK(cudaEventRecord(h->ev[1], st), "event");
+
+  const fram_schedule& sch = h->sched;
+  const bool replay = !h->replay.empty();
+  const int T = replay ? (int)h->replay.size() : sch.max_outer;
+  double* scal = h->scal.as<double>();
+  double ms_gemm = 0, ms_sdsn = 0, ms_update = 0;
+  int t = 0, capped = 0;
+  int64_t total = 0;
+  bool converged = false;
+  fram::ShardSdsnParams sp{};
+  sp.Y = h->Y.p; sp.rows = m; sp.n = n; sp.ld = ld;
+  sp.theta = sch.theta; sp.gamma_th = sch.gamma_th; sp.sdsn_max = sch.sdsn_max;
+  sp.scale = (sch.flags & FRAM_FLAG_NO_THETA_SCALE) ? 0 : 1;
+  sp.colpart = h->shColpart.p; sp.rsum = h->shRsum.as<double>();
+  sp.send = h->shSend.as<double>(); sp.recv = h->shRecv.as<double>();
+  sp.gamma_hist = h->ghist.as<double>();
+  sp.state = h->shState.as<fram::ShardSdsnState>();
+  fram::ShardSdsnState hstate{};
+  for (t = 1; t <= T; ++t) {
+    if (timing) CK(cudaEventRecord(h->ev[2], st), "event");
+    // gradient: U_rᵀ (n × m), all-gather, G_r = A'_r · U + λK'_r
+    fram::GemmArgs g1{f64 ? h->N.p : h->Nq.p, h->BqT.p, m, n, n, ld, 0, h->shUT.p, m, nullptr, 0.0};
+    if (f64) CK(fram::launch_gemm_f64(g1, st), "gemm1 f64"); else CK(fram::launch_gemm_tc(g1, op, st), "gemm1 tcgen05");
+    if (nck(fram::shard_allgather_bytes(sh, h->shUT.p, h->shUblk.p, (size_t)n * m * es, st, &err)) != FRAM_OK)
+      return FRAM_ERR_NCCL;
+    fram::GemmArgs g2{h->Aq.p, h->shUblk.p, m, n, n, ld, 1, h->Y.p, ld, dK ? h->Kq.p : nullptr, h->lambda};
+    g2.kchunk = m;
+    if (f64) CK(fram::launch_gemm_f64(g2, st), "gemm2 f64"); else CK(fram::launch_gemm_tc(g2, op, st), "gemm2 tcgen05");
+    h->launches += 2;
+    if (timing) CK(cudaEventRecord(h->ev[3], st), "event");
+    // SDSN on the row block
+    sp.sdsn_fixed = replay ? h->replay[t - 1] : sch.sdsn_fixed;
+    CK(cudaMemsetAsync(sp.state, 0, sizeof(fram::ShardSdsnState), st), "state reset");
+    CK(fram::launch_sdsn_sh_max(sp, f64, st, h->num_sms), "sdsn max");
+    if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, 1, true, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
+    CK(fram::launch_sdsn_sh_sweep(sp, f64, 0, 0, st, h->num_sms), "sdsn scale");
+    if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
+    h->launches += 5;
+    const int cap = std::max(1, sp.sdsn_fixed > 0 ? sp.sdsn_fixed : sch.sdsn_max);
+    constexpr int kChunk = 16;                         // passes queued between host polls of `done`
+    for (int p0 = 0; p0 < cap; p0 += kChunk) {
+      for (int p = p0; p < std::min(cap, p0 + kChunk); ++p) {
+        CK(fram::launch_sdsn_sh_sweep(sp, f64, 1, p, st, h->num_sms), "sdsn pass");
+        if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK)
+          return FRAM_ERR_NCCL;
+        h->launches += 3;
+      }
+      CK(cudaMemcpyAsync(&hstate, sp.state, sizeof(hstate), cudaMemcpyDeviceToHost, st), "state readback");
+      CK(cudaStreamSynchronize(st), "state sync");
+      if (hstate.done) break;
+    }
+    if (!hstate.done) return fail(FRAM_ERR_CUDA, "sharded SDSN did not finish");
+    if (timing) CK(cudaEventRecord(h->ev[4], st), "event");
+    CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, m, n, ld, sch.alpha, h->upd.as<double>(),
+                           reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8), scal + 4, st,
+                           h->num_sms),
+       "update");
+    h->launches++;
+    if (nck(fram::shard_allreduce_f64(sh, scal + 4, scal + 12, 2, false, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
+    if (timing) CK(cudaEventRecord(h->ev[5], st), "event");
+    CK(cudaMemcpyAsync(h->hscal, scal, kScalDoubles * 8, cudaMemcpyDeviceToHost, st), "scalar readback");
+    CK(cudaStreamSynchronize(st), "iteration sync");
+    const int passes = hstate.passes;
+    const double delta = std::sqrt(h->hscal[12]) / std::sqrt(h->hscal[13]);   // same formula as K5
+    if (!std::isfinite(delta)) return fail(FRAM_ERR_DATA, "non-finite delta (overflow in the gradient?)");
+    total += passes;
+    if (sp.sdsn_fixed == 0 && passes >= sch.sdsn_max) ++capped;
+    if (timing) {
+      float a, b, cc;
+      cudaEventElapsedTime(&a, h->ev[2], h->ev[3]);
+      cudaEventElapsedTime(&b, h->ev[3], h->ev[4]);
+      cudaEventElapsedTime(&cc, h->ev[4], h->ev[5]);
+      ms_gemm += a; ms_sdsn += b; ms_update += cc;
+    }
+    if (stats && (sch.flags & FRAM_FLAG_TRACE)) {
+      if (stats->passes_per_iter) stats->passes_per_iter[t - 1] = passes;
+      if (stats->delta_trace) stats->delta_trace[t - 1] = delta;
+      if (stats->gamma_last) stats->gamma_last[t - 1] = hstate.gamma_last;
+    }
+    if (delta <= sch.delta_th) {
+      converged = true;
+      if (!replay) break;
+    } else if (replay) {
+      converged = false;
+    }
+  }
+  if (t > T) t = T;
+  // discretisation: all ranks gather N and run the same deterministic LAP (R17)
+  if (timing) CK(cudaEventRecord(h->ev[6], st), "event");
+  if (nck(fram::shard_allgather_bytes(sh, h->N.p, h->shNfull.p, (size_t)m * ld * 8, st, &err)) != FRAM_OK)
+    return FRAM_ERR_NCCL;
+  CK(fram::launch_lap(h->shNfull.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
+  h->launches++;
+  if (timing) CK(cudaEventRecord(h->ev[7], st), "event");
+  if (X_out) CK(cudaMemcpy2DAsync(X_out, n * 8, h->N.p, ld * 8, n * 8, m, cudaMemcpyDefault, st), "X_out copy");
+  if (perm_out) CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
+  CK(cudaStreamSynchronize(st), "final sync");
+  if (stats) {
+    stats->outer_iters = t;
+    stats->converged = converged ? 1 : 0;
+    stats->sdsn_capped_calls = capped;
+    stats->total_passes = total;
+    stats->kernel_launches = h->launches;
+    stats->sdsn_kernel = 3;
+    if (timing) {
+      float a, b, cc;
+      cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);
+      cudaEventElapsedTime(&b, h->ev[6], h->ev[7]);
+      cudaEventElapsedTime(&cc, h->ev[0], h->ev[7]);
+      stats->ms_precond = a; stats->ms_lap = b; stats->ms_total = cc;
+      stats->ms_gemm = ms_gemm; stats->ms_sdsn = ms_sdsn; stats->ms_update = ms_update;
+    }
+  }
+  if (!converged) {
+    g_err = "max_outer reached without delta <= delta_th";
+    return FRAM_NOT_CONVERGED;
+  }
+  return FRAM_OK;
 }
 
 }  // namespace
@@ -350,7 +546,8 @@ void fram_destroy(fram_handle h) {
   cudaSetDevice(h->device);
   DevBuf* bufs[] = {&h->Aq, &h->BqT, &h->Kq, &h->N, &h->Nq, &h->UT, &h->Y, &h->colpart, &h->Spart, &h->Mpart,
                     &h->cvec, &h->bar, &h->scal, &h->ghist, &h->upd, &h->lapw, &h->permd, &h->stA, &h->stB,
-                    &h->stK, &h->stX0, &h->stX, &h->scan, &h->rcolpart, &h->rbvec, &h->rflags, &h->rdbg};
+                    &h->stK, &h->stX0, &h->stX, &h->scan, &h->rcolpart, &h->rbvec, &h->rflags, &h->rdbg, &h->shUT, &h->shUblk, &h->shRsum,
+                    &h->shSend, &h->shRecv, &h->shState, &h->shNfull, &h->shColpart, &h->shScan};
   for (DevBuf* b : bufs) b->release();
   if (h->hscal) cudaFreeHost(h->hscal);
   for (auto& e : h->ev)
@@ -369,6 +566,9 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (!A || !B) return fail(FRAM_ERR_USAGE, "A and B are required");
+  if (h->shard)
+    return sharded_solve(h, (int)dt, A, B, K, X0, (int)p, reinterpret_cast<cudaStream_t>(stream), X_out, perm_out,
+                         stats);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int op = prec_to_op(p);
   const bool f64 = (op == 0);
@@ -389,7 +589,7 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
 
   double c = 0;
   if ((rs = precondition(h, (int)dt, dA, dB, dK, op, st, &c)) != FRAM_OK) return rs;
-  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dX0, n, ld, st), "init N");
+  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dX0, n, n, ld, st), "init N");
   h->launches++;
   if (timing) CK(cudaEventRecord(h->ev[1], st), "event");
 
@@ -408,7 +608,7 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     const int fixed = replay ? h->replay[t - 1] : sc.sdsn_fixed;
     if ((rs = run_sdsn(h, f64, fixed, st)) != FRAM_OK) return rs;
     if (timing) CK(cudaEventRecord(h->ev[4], st), "event");
-    CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, n, ld, sc.alpha, h->upd.as<double>(),
+    CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, n, n, ld, sc.alpha, h->upd.as<double>(),
                            reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8), scal + 4, st,
                            h->num_sms),
        "update");
@@ -483,6 +683,7 @@ fram_status fram_sdsn(fram_handle h, fram_precision p, const void* X, void* D_ou
                       double* gamma_hist, void* stream) {
   fram_status s0 = common_checks(h, 0, p);
   if (s0 != FRAM_OK) return s0;
+  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   if (!X || !D_out || !passes) return fail(FRAM_ERR_USAGE, "X, D_out and passes are required");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool f64 = (p == FRAM_PREC_FP64);
@@ -517,6 +718,7 @@ fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, const voi
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (!A || !B || !Nin || !G_out) return fail(FRAM_ERR_USAGE, "A, B, N and G_out are required");
+  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int op = prec_to_op(p);
   const long n = h->n, ld = h->ld;
@@ -531,7 +733,7 @@ fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, const voi
   if ((rs = stage_in(h, h->stX0, Nin, (size_t)n * n * 8, st, &dN)) != FRAM_OK) return rs;
   double c = 0;
   if ((rs = precondition(h, (int)dt, dA, dB, dK, op, st, &c)) != FRAM_OK) return rs;
-  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dN, n, ld, st), "init N");
+  CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dN, n, n, ld, st), "init N");
   if ((rs = gradient(h, op, dK != nullptr, st)) != FRAM_OK) return rs;
   const size_t es = op == 0 ? 8 : 4;
   CK(cudaMemcpy2DAsync(G_out, n * es, h->Y.p, ld * es, n * es, n, cudaMemcpyDefault, st), "G copy");
@@ -543,6 +745,7 @@ fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, const voi
 fram_status fram_lap(fram_handle h, const double* Nin, int32_t* perm_out, void* stream) {
   fram_status s0 = common_checks(h, 0, FRAM_PREC_FP64);
   if (s0 != FRAM_OK) return s0;
+  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   if (!Nin || !perm_out) return fail(FRAM_ERR_USAGE, "N and perm_out are required");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const long n = h->n, ld = h->ld;
@@ -562,6 +765,7 @@ fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype dt, cons
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (batch < 0 || !A || !B) return fail(FRAM_ERR_USAGE, "bad batch arguments");
+  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   std::string err;
   fram_status s = fram::batched_solve(h->bws, h->n, h->lambda, h->sched, batch, (int)dt, A, B, K, X0, (int)p,
                                       reinterpret_cast<cudaStream_t>(stream), X_out, perm_out, status_out, stats,

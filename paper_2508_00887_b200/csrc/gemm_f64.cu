@@ -28,7 +28,7 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
 
 __global__ void __launch_bounds__(THREADS) gemm_f64_kernel(const double* __restrict__ A, const double* __restrict__ B,
                                                            long M, long N, long K, long ld, int epi, double* out,
-                                                           long ldo, const double* Kq, double lam) {
+                                                           long ldo, const double* Kq, double lam, long kchunk) {
   __shared__ __align__(16) double As[2][TM][PADK];
   __shared__ __align__(16) double Bs[2][TN][PADK];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -51,7 +51,8 @@ __global__ void __launch_bounds__(THREADS) gemm_f64_kernel(const double* __restr
       cp_async16(&As[buf][r][kc], ok ? (const void*)(A + gr * ld + gk) : (const void*)A, ok);
       const long gn = n0 + r;
       const bool okb = gn < N && gk < K;
-      cp_async16(&Bs[buf][r][kc], okb ? (const void*)(B + gn * ld + gk) : (const void*)B, okb);
+      const double* bp = kchunk ? B + (gk / kchunk) * N * kchunk + gn * kchunk + gk % kchunk : B + gn * ld + gk;
+      cp_async16(&Bs[buf][r][kc], okb ? (const void*)bp : (const void*)B, okb);
     }
     cp_commit();
   };
@@ -100,7 +101,7 @@ __global__ void __launch_bounds__(THREADS) gemm_f64_kernel(const double* __restr
 cudaError_t launch_gemm_f64(const GemmArgs& g, cudaStream_t st) {
   dim3 grid((unsigned)((g.N + TN - 1) / TN), (unsigned)((g.M + TM - 1) / TM));
   gemm_f64_kernel<<<grid, THREADS, 0, st>>>((const double*)g.Aop, (const double*)g.Bop, g.M, g.N, g.K, g.ld, g.epi,
-                                            (double*)g.out, g.ldo, (const double*)g.Kq, g.lam);
+                                            (double*)g.out, g.ldo, (const double*)g.Kq, g.lam, g.kchunk);
   return cudaGetLastError();
 }
 

@@ -43,6 +43,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
   } while (!ok);
 }
+__device__ __forceinline__ void tma_load_3d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y, int z) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst, int x, int y) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
@@ -98,6 +104,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 
 struct EpiArgs {
   long M, N, K;
+  long kchunk;   // > 0: B operand K-blocked (3-D tensor map: {kchunk, N, K/kchunk})
   int epi;
   void* out;
   long ldo;
@@ -158,7 +165,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         mbar_wait(empty + s, ph ^ 1u);
         mbar_expect_tx(full + s, STAGE_BYTES);
         tma_load_2d(&tmA, full + s, sA + s * TILE_A, kb * BK, m0);
-        tma_load_2d(&tmB, full + s, sB + s * TILE_B, kb * BK, n0);
+        if (ea.kchunk > 0) {
+          const long k0 = (long)kb * BK;
+          tma_load_3d(&tmB, full + s, sB + s * TILE_B, (int)(k0 % ea.kchunk), n0, (int)(k0 / ea.kchunk));
+        } else {
+          tma_load_2d(&tmB, full + s, sB + s * TILE_B, kb * BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
@@ -260,12 +272,33 @@ bool make_map(CUtensorMap* m, const void* base, int op, long rows, long kdim, lo
   return r == CUDA_SUCCESS;
 }
 
+// K-blocked operand: {kchunk, rows, K/kchunk}, 128B-swizzled boxes of {128 B of K, box_rows, 1}
+bool make_map_blocked(CUtensorMap* m, const void* base, int op, long rows, long kdim, long kchunk, int box_rows) {
+  EncodeTiledFn enc = get_encode();
+  if (!enc || kchunk <= 0 || kdim % kchunk) return false;
+  const int esz = (op == 1) ? 4 : 2;
+  CUtensorMapDataType dt = (op == 1) ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                     : (op == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+  cuuint64_t gdim[3] = {(cuuint64_t)kchunk, (cuuint64_t)rows, (cuuint64_t)(kdim / kchunk)};
+  cuuint64_t gstride[2] = {(cuuint64_t)(kchunk * esz), (cuuint64_t)(rows * kchunk * esz)};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / esz), (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(m, dt, 3, const_cast<void*>(base), gdim, gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 template <int OP>
 cudaError_t launch_op(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap ta, tb;
   if (!make_map(&ta, g.Aop, OP, g.M, g.K, g.ld, BM)) return cudaErrorInvalidValue;
-  if (!make_map(&tb, g.Bop, OP, g.N, g.K, g.ld, BN)) return cudaErrorInvalidValue;
-  EpiArgs ea{g.M, g.N, g.K, g.epi, g.out, g.ldo, reinterpret_cast<const float*>(g.Kq), (float)g.lam};
+  if (g.kchunk > 0) {
+    if (g.kchunk % (128 / ((OP == 1) ? 4 : 2)) || !make_map_blocked(&tb, g.Bop, OP, g.N, g.K, g.kchunk, BN))
+      return cudaErrorInvalidValue;
+  } else if (!make_map(&tb, g.Bop, OP, g.N, g.K, g.ld, BN)) {
+    return cudaErrorInvalidValue;
+  }
+  EpiArgs ea{g.M, g.N, g.K, g.kchunk, g.epi, g.out, g.ldo, reinterpret_cast<const float*>(g.Kq), (float)g.lam};
   auto fn = gemm_tc_kernel<OP>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;

@@ -50,6 +50,31 @@ long sdsn_res_slots(long n);
 size_t sdsn_res_xchg_words(long n, int num_sms);   // size of ResParams::xchg
 cudaError_t launch_sdsn_resident(const ResParams& p, cudaStream_t st, int num_sms);
 
+// ---- K4s: SDSN on a row block for the sharded solve (per-pass kernels + host NCCL all-reduce) ----
+struct ShardSdsnState {
+  int done, done_pending, passes, _pad;
+  double gamma_last, maxx, S_last;
+};
+struct ShardSdsnParams {
+  void* Y;             // rows×ld, T (float mixed, double FP64), in place
+  long rows, n, ld;
+  double theta, gamma_th;
+  int sdsn_max, sdsn_fixed, scale;
+  void* colpart;       // [grid][ld] T
+  double* rsum;        // [rows] local row sums of the current iterate (FP64)
+  double* send;        // [n+1] local column sums, local mass (and [0] = local max in the max phase)
+  double* recv;        // [n+1] all-reduced (sum; max in the max phase)
+  double* gamma_hist;  // nullable, [sdsn_max]
+  ShardSdsnState* state;
+};
+int sdsn_sh_grid(long rows, int num_sms, bool f64);
+size_t sdsn_sh_smem(long ld, bool f64);
+cudaError_t launch_sdsn_sh_max(const ShardSdsnParams& p, bool f64, cudaStream_t st, int num_sms);
+// mode 0: scale sweep (after the max all-reduce), mode 1: pass `pass`; both end with the local
+// column/mass reduction into p.send (the caller all-reduces send → recv)
+cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, int pass, cudaStream_t st,
+                                 int num_sms);
+
 // ---- K1: preconditioning (Alg.1 steps 2-3) ------------------------------------
 // in_dt: 0 f64, 1 f32, 2 bf16.  op: 0 f64, 1 tf32 (stored f32), 2 bf16, 3 fp16.
 struct PrecondScan {        // device-side result of the validation / max scan
@@ -59,27 +84,37 @@ struct PrecondScan {        // device-side result of the validation / max scan
 cudaError_t launch_precond_scan(const void* A, const void* B, const void* K, int in_dt, long n,
                                 bool check_sym, PrecondScan* out_dev, double* blockbuf,
                                 unsigned* counter, cudaStream_t st);
-// A' = A/√c → op (row-major, ld), Bt' = (Ã/√c)ᵀ → op (row-major, ld), K' = K/c → kdst (f32 or f64)
+// accumulate max / non-finite / negative counts of the rows × n blocks A and K into *out_dev
+// (no memset; no symmetry test — a row block cannot see its transpose)
+cudaError_t launch_precond_scan_rows(const void* A, const void* K, int in_dt, long rows, long n,
+                                     PrecondScan* out_dev, cudaStream_t st);
+// A' = A/√c → op (row-major, ld), Bt' = (Ã/√c)ᵀ → op (row-major, ld), K' = K/c → kdst (f32 or f64);
+// A and K have rows_a rows (n, or n/W for a shard), Ã is n × n
 cudaError_t launch_precond_apply(const void* A, const void* B, const void* K, int in_dt, long n,
                                  long ld, const double* c_dev, int op, void* Aq, void* BqT,
-                                 void* Kq, bool k_f64, cudaStream_t st);
+                                 void* Kq, bool k_f64, cudaStream_t st, long rows_a = -1);
 
 // ---- K2/K3: gradient GEMMs ------------------------------------------------------------------
 // D[M×N] = Aop[M×K] · Bop[N×K]ᵀ (both row-major, K contiguous, leading dim ld).
 // epi 0: OutT[j*ldo + i] = round_op(D[i][j])  (transposed store in the operand format)
 // epi 1: G[i*ldo + j] = D[i][j] + lam*Kq[i*ldo + j]  (FP32 G; Kq nullable)
+// kchunk > 0: Bop is K-blocked — K/kchunk chunks of (N × kchunk) row-major matrices, element (j, k)
+// at Bop[(k / kchunk)·N·kchunk + j·kchunk + k % kchunk] (the all-gathered Uᵀ blocks of a sharded
+// solve); kchunk must divide K and be a multiple of 64.
 struct GemmArgs {
   const void* Aop; const void* Bop; long M, N, K, ld;
   int epi; void* out; long ldo; const void* Kq; double lam;
+  long kchunk = 0;
 };
 cudaError_t launch_gemm_tc(const GemmArgs& g, int op, cudaStream_t st);     // tcgen05 (op 1,2,3)
 cudaError_t launch_gemm_f64(const GemmArgs& g, cudaStream_t st);            // DMMA FP64
 
 // ---- K5/K6: update N ← (1−α)N + αD, N_q, δ (Alg.1 steps 7-8) --------------------------------
-cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long n, long ld,
+// rows × n blocks (rows = n for a full solve; n/W for a shard)
+cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long rows, long n, long ld,
                           double alpha, double* partials, unsigned* counter, double* out3,
                           cudaStream_t st, int num_sms);
-cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long n, long ld,
+cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long rows, long n, long ld,
                           cudaStream_t st);
 
 // ---- K7: LAP (Alg.1 step 10, R17) --------------------------------------------------------------

@@ -104,10 +104,37 @@ template <> __device__ __forceinline__ __nv_bfloat16 to_op<2>(double x) { return
 template <> __device__ __forceinline__ __half to_op<3>(double x) { return __double2half(x); }
 
 // A' (row-major) and Ã'ᵀ (row-major) into ld-padded buffers; K' = K/c (f32 or f64).
+__global__ void precond_scan_rows_kernel(const void* A, const void* K, int dt, long rows, long n,
+                                         PrecondScan* out) {
+  const void* mats[2] = {A, K};
+  for (int mi = 0; mi < 2; ++mi) {
+    const void* M = mats[mi];
+    if (!M) continue;
+    double mx = 0.0;
+    unsigned long long nf = 0, ng = 0;
+    for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < rows * n; idx += (long)gridDim.x * blockDim.x) {
+      const double v = load_as_f64(M, dt, idx);
+      if (!isfinite(v)) ++nf;
+      else if (v < 0.0) ++ng;
+      else mx = fmax(mx, v);
+    }
+    mx = warp_max_d(mx);
+    if ((threadIdx.x & 31) == 0) atomic_max_nonneg(&out->maxv[mi == 0 ? 0 : 2], mx);
+    if (nf) atomicAdd(&out->bad_nonfinite, nf);
+    if (ng) atomicAdd(&out->bad_negative, ng);
+  }
+}
+
+cudaError_t launch_precond_scan_rows(const void* A, const void* K, int in_dt, long rows, long n,
+                                     PrecondScan* out_dev, cudaStream_t st) {
+  precond_scan_rows_kernel<<<296, 256, 0, st>>>(A, K, in_dt, rows, n, out_dev);
+  return cudaGetLastError();
+}
+
 template <int OP>
 __global__ void precond_apply_kernel(const void* A, const void* B, const void* K, int dt, long n,
                                      long ld, const double* cmax, void* Aq, void* BqT, void* Kq,
-                                     int k_f64) {
+                                     int k_f64, long rows_a) {
   using OT = typename OpT<OP>::t;
   __shared__ double tb[32][33];
   const double c = fmax(fmax(cmax[0], cmax[1]), cmax[2]);
@@ -119,11 +146,13 @@ __global__ void precond_apply_kernel(const void* A, const void* B, const void* K
   for (int r = ty; r < 32; r += 8) {
     const long i = ti * 32 + r, j = tj * 32 + tx;
     if (i < n && j < n) {
-      aq[i * ld + j] = to_op<OP>(load_as_f64(A, dt, i * n + j) / sA);
-      if (K) {
-        const double kv = load_as_f64(K, dt, i * n + j) / c;
-        if (k_f64) reinterpret_cast<double*>(Kq)[i * ld + j] = kv;
-        else reinterpret_cast<float*>(Kq)[i * ld + j] = __double2float_rn(kv);
+      if (i < rows_a) {
+        aq[i * ld + j] = to_op<OP>(load_as_f64(A, dt, i * n + j) / sA);
+        if (K) {
+          const double kv = load_as_f64(K, dt, i * n + j) / c;
+          if (k_f64) reinterpret_cast<double*>(Kq)[i * ld + j] = kv;
+          else reinterpret_cast<float*>(Kq)[i * ld + j] = __double2float_rn(kv);
+        }
       }
       tb[r][tx] = load_as_f64(B, dt, i * n + j) / sA;
     }
@@ -137,15 +166,16 @@ __global__ void precond_apply_kernel(const void* A, const void* B, const void* K
 
 cudaError_t launch_precond_apply(const void* A, const void* B, const void* K, int in_dt, long n,
                                  long ld, const double* c_dev, int op, void* Aq, void* BqT,
-                                 void* Kq, bool k_f64, cudaStream_t st) {
+                                 void* Kq, bool k_f64, cudaStream_t st, long rows_a) {
+  if (rows_a < 0) rows_a = n;
   const long nt = (n + 31) / 32;
   dim3 grid((unsigned)nt, (unsigned)nt), block(32, 8);
   const int kf = k_f64 ? 1 : 0;
   switch (op) {
-    case 0: precond_apply_kernel<0><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf); break;
-    case 1: precond_apply_kernel<1><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf); break;
-    case 2: precond_apply_kernel<2><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf); break;
-    case 3: precond_apply_kernel<3><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf); break;
+    case 0: precond_apply_kernel<0><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf, rows_a); break;
+    case 1: precond_apply_kernel<1><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf, rows_a); break;
+    case 2: precond_apply_kernel<2><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf, rows_a); break;
+    case 3: precond_apply_kernel<3><<<grid, block, 0, st>>>(A, B, K, in_dt, n, ld, c_dev, Aq, BqT, Kq, kf, rows_a); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

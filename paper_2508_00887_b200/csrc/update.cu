@@ -26,13 +26,13 @@ template <> __device__ __forceinline__ void store_op<3>(void* p, long idx, doubl
 
 template <int OP, typename TD>
 __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict__ N, const TD* __restrict__ D,
-                                                             void* Nq, long n, long ld, double alpha,
+                                                             void* Nq, long rows, long n, long ld, double alpha,
                                                              double* partials, unsigned* counter, double* out3) {
   __shared__ double s1[UPD_THREADS / 32], s2[UPD_THREADS / 32];
   __shared__ bool is_last;
   const double oma = 1.0 - alpha;
   double dd = 0.0, nn = 0.0;
-  for (long i = blockIdx.x; i < n; i += gridDim.x) {
+  for (long i = blockIdx.x; i < rows; i += gridDim.x) {
     double* nr = N + i * ld;
     const TD* dr = D + i * ld;
     for (long j = threadIdx.x; j < n; j += UPD_THREADS) {
@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict_
 }
 
 template <int OP>
-__global__ void init_n_kernel(double* N, void* Nq, const double* X0, long n, long ld) {
+__global__ void init_n_kernel(double* N, void* Nq, const double* X0, long rows, long n, long ld) {
   const double u = 1.0 / (double)n;
-  for (long i = blockIdx.x; i < n; i += gridDim.x)
+  for (long i = blockIdx.x; i < rows; i += gridDim.x)
     for (long j = threadIdx.x; j < n; j += blockDim.x) {
       const double v = X0 ? X0[i * n + j] : u;
       N[i * ld + j] = v;
@@ -89,13 +89,14 @@ __global__ void copy2d_kernel(double* dst, long ldd, const double* src, long lds
 
 }  // namespace
 
-cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long n, long ld, double alpha,
-                          double* partials, unsigned* counter, double* out3, cudaStream_t st, int num_sms) {
-  const int grid = (int)((n < (long)num_sms * 4) ? n : (long)num_sms * 4);
+cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long rows, long n, long ld,
+                          double alpha, double* partials, unsigned* counter, double* out3, cudaStream_t st,
+                          int num_sms) {
+  const int grid = (int)((rows < (long)num_sms * 4) ? rows : (long)num_sms * 4);
 #define UPD_CASE(OPV)                                                                                        \
-  if (d_f64) update_kernel<OPV, double><<<grid, UPD_THREADS, 0, st>>>(N, (const double*)D, Nq, n, ld, alpha, \
+  if (d_f64) update_kernel<OPV, double><<<grid, UPD_THREADS, 0, st>>>(N, (const double*)D, Nq, rows, n, ld, alpha, \
                                                                     partials, counter, out3);                \
-  else update_kernel<OPV, float><<<grid, UPD_THREADS, 0, st>>>(N, (const float*)D, Nq, n, ld, alpha,         \
+  else update_kernel<OPV, float><<<grid, UPD_THREADS, 0, st>>>(N, (const float*)D, Nq, rows, n, ld, alpha,         \
                                                              partials, counter, out3);
   switch (op) {
     case 0: UPD_CASE(0) break;
@@ -108,13 +109,14 @@ cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op
   return cudaGetLastError();
 }
 
-cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long n, long ld, cudaStream_t st) {
-  const int grid = (int)(n < 1024 ? n : 1024);
+cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long rows, long n, long ld,
+                          cudaStream_t st) {
+  const int grid = (int)(rows < 1024 ? rows : 1024);
   switch (op) {
-    case 0: init_n_kernel<0><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
-    case 1: init_n_kernel<1><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
-    case 2: init_n_kernel<2><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
-    case 3: init_n_kernel<3><<<grid, 256, 0, st>>>(N, Nq, X0, n, ld); break;
+    case 0: init_n_kernel<0><<<grid, 256, 0, st>>>(N, Nq, X0, rows, n, ld); break;
+    case 1: init_n_kernel<1><<<grid, 256, 0, st>>>(N, Nq, X0, rows, n, ld); break;
+    case 2: init_n_kernel<2><<<grid, 256, 0, st>>>(N, Nq, X0, rows, n, ld); break;
+    case 3: init_n_kernel<3><<<grid, 256, 0, st>>>(N, Nq, X0, rows, n, ld); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

@@ -161,11 +161,14 @@ def _like(ref, shape, kind):
 
 
 class Handle:
-    """Owns a fram_handle (fram_create / fram_destroy)."""
+    """Owns a fram_handle (fram_create / fram_destroy).  `rows` = n, or n/W for a sharded handle."""
 
-    def __init__(self, ptr, n):
+    def __init__(self, ptr, n, rows=None, rank=0, world=1):
         self.ptr = ptr
         self.n = n
+        self.rows = n if rows is None else rows
+        self.rank = rank
+        self.world = world
 
     def __del__(self):
         try:
@@ -211,7 +214,7 @@ def fram_solve(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, 
                max_outer=1000):
     """Alg. 1 end to end.  Returns (status, stats, X_out, perm_out); raises FramError on errors."""
     n = h.n
-    X_out = _like(A, (n, n), "f64") if X_out is None else X_out
+    X_out = _like(A, (h.rows, n), "f64") if X_out is None else X_out
     perm_out = _like(A, (n,), "i32") if perm_out is None else perm_out
     arrays = ((C.c_int32 * max_outer)(), (C.c_double * max_outer)(), (C.c_double * max_outer)())
     st = _Stats()
@@ -291,12 +294,54 @@ def fram_get_unique_id() -> bytes:
 
 
 def fram_create_sharded(n, lam, schedule: Schedule | None, uid: bytes, rank, world, device=0) -> Handle:
+    """Row-sharded handle (rank owns rows [rank·n/W, (rank+1)·n/W)); `uid` from fram_get_unique_id on one
+    rank, shared with all (see create_sharded_dist)."""
     s, keep = (schedule or Schedule()).to_c()
     out = C.c_void_p()
     _check(lib().fram_create_sharded(int(n), float(lam), C.byref(s), uid, int(rank), int(world), int(device),
                                      C.byref(out)))
     del keep
-    return Handle(out, int(n))
+    return Handle(out, int(n), rows=int(n) // int(world), rank=int(rank), world=int(world))
+
+
+def shard_rows(n, rank, world):
+    """Row range [r0, r1) owned by `rank` in a sharded solve (n % world == 0)."""
+    if n % world:
+        raise ValueError("n must be divisible by the number of ranks")
+    m = n // world
+    return rank * m, (rank + 1) * m
+
+
+def broadcast_unique_id(make_id, group=None, src=0):
+    """Rank `src` calls make_id() (fram_get_unique_id for real runs), the 128 bytes are broadcast over
+    torch.distributed (CPU tensor: works for gloo and nccl process groups).  Returns bytes."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    buf = torch.zeros(128, dtype=torch.uint8)
+    if rank == src:
+        raw = make_id()
+        if len(raw) != 128:
+            raise ValueError("unique id must be 128 bytes")
+        buf.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+    if dist.get_backend(group) == "nccl":
+        dev = torch.device("cuda", torch.cuda.current_device())
+        g = buf.to(dev)
+        dist.broadcast(g, src, group=group)
+        buf = g.cpu()
+    else:
+        dist.broadcast(buf, src, group=group)
+    return bytes(buf.numpy().tobytes())
+
+
+def create_sharded_dist(n, lam=1.0, schedule: Schedule | None = None, group=None, device=None) -> Handle:
+    """fram_create_sharded for the calling torch.distributed rank (one process per GPU)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    dev = torch.cuda.current_device() if device is None else device
+    uid = broadcast_unique_id(fram_get_unique_id, group=group)
+    return fram_create_sharded(n, lam, schedule, uid, rank, world, device=dev)
 
 
 def fram_build_info() -> str:
