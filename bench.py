@@ -43,6 +43,10 @@ def parse():
     p.add_argument("--n", type=int, default=4096, help="dev override (the metric is quoted at 4096)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                   help="c4: the metric's config (n=4096, replicas across ranks); c5: n=16384 row-sharded "
+                        "across the ranks (NCCL), not part of the default run")
+    p.add_argument("--max-outer", type=int, default=None, help="c5: cap on outer iterations per solve (bounded runs)")
     return p.parse_args()
 
 
@@ -354,10 +358,88 @@ def run_ours(args):
     return 0
 
 
+def run_c5(args):
+    """C5 (BASELINE configs[4]): weighted ER n=16384, rows of A, G and N sharded across the ranks
+    (fram_create_sharded; NCCL all-gather of the Uᵀ blocks per outer iteration and an all-reduce of
+    the column sums per SDSN pass).  `value` = outer iterations of the one sharded solve ÷ max-over-ranks
+    device time ("scaling": "strong": the problem is fixed as the rank count grows)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_00887_b200 as fb
+    from synth import config_c5
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n = 16384 if args.n == 4096 else args.n
+    inst = config_c5(0, n=n)
+    r0, r1 = fb.shard_rows(n, rank, world)
+    A = torch.tensor(inst.A[r0:r1], dtype=torch.bfloat16, device=dev)      # C5 is stored dense BF16
+    B = torch.tensor(inst.B, dtype=torch.bfloat16, device=dev)
+    flags = fb.FLAG_TRACE | fb.FLAG_TIME_PHASES
+    sch = fb.Schedule(theta=inst.theta, alpha=SCHEDULE["alpha"], gamma_th=SCHEDULE["gamma_th"],
+                      delta_th=SCHEDULE["delta_th"], max_outer=args.max_outer or SCHEDULE["max_outer"],
+                      sdsn_max=SCHEDULE["sdsn_max"], flags=flags)
+    if world > 1:
+        h = fb.create_sharded_dist(n, lam=SCHEDULE["lam"], schedule=sch)
+    else:
+        h = fb.fram_create_sharded(n, SCHEDULE["lam"], sch, fb.fram_get_unique_id(), 0, 1, device=local)
+    X = torch.empty((r1 - r0, n), dtype=torch.float64, device=dev)
+    perm = torch.empty((n,), dtype=torch.int32, device=dev)
+    for _ in range(args.warmup):
+        fb.fram_solve(h, A, B, precision=args.precision, X_out=X, perm_out=perm)
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    tot_ms, stats = 0.0, []
+    for k in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        _, s, _, _ = fb.fram_solve(h, A, B, precision=args.precision, X_out=X, perm_out=perm)
+        b.record()
+        b.synchronize()
+        tot_ms += a.elapsed_time(b)
+        stats.append(s)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    clocks = sampler.stop()
+    iters = sum(s["outer_iters"] for s in stats)
+    passes = sum(s["total_passes"] for s in stats)
+    if rank == 0:
+        acc = float((perm.cpu().numpy() == inst.perm_true).mean())
+        line = {"metric": METRIC, "value": iters / (tot_ms / 1e3), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "bf16-gemm/f32-sdsn/f64-update", "data": "synthetic (seeded C5 generator)",
+                "config": {"workload": "C5: weighted ER(p=0.01) n=16384, BF16 storage, 5% rewiring, rows sharded",
+                           "n": n, "precision": args.precision, "schedule": dict(SCHEDULE, max_outer=sch.max_outer),
+                           "parallelism": f"row-sharded over {world} rank(s) (NCCL)"},
+                "outer_iters_per_solve": iters / args.steps, "mean_passes_per_iter": passes / max(iters, 1),
+                "accuracy": acc, "sdsn_us_per_pass": 1e3 * sum(s["ms_sdsn"] for s in stats) / max(passes, 1),
+                "gemm_ms_per_iter": sum(s["ms_gemm"] for s in stats) / max(iters, 1),
+                "lap_ms_per_step": sum(s["ms_lap"] for s in stats) / args.steps,
+                "gpu_launches": sum(s["kernel_launches"] for s in stats), "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "c5":
+        return run_c5(args)
     return run_ours(args)
 
 
