@@ -43,9 +43,10 @@ def parse():
     p.add_argument("--n", type=int, default=4096, help="dev override (the metric is quoted at 4096)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    p.add_argument("--workload", default="c4", choices=["c4", "c5"],
-                   help="c4: the metric's config (n=4096, replicas across ranks); c5: n=16384 row-sharded "
-                        "across the ranks (NCCL), not part of the default run")
+    p.add_argument("--workload", default="c4", choices=["c4", "c3", "c5"],
+                   help="c4: the metric's config (n=4096, replicas across ranks); c3: 4096 keypoint instances "
+                        "(n=64) split across the ranks, one CTA per instance; c5: n=16384 row-sharded across "
+                        "the ranks (NCCL).  c3/c5 are not part of the default run")
     p.add_argument("--max-outer", type=int, default=None, help="c5: cap on outer iterations per solve (bounded runs)")
     return p.parse_args()
 
@@ -434,12 +435,81 @@ def run_c5(args):
     return 0
 
 
+def run_c3(args):
+    """C3 (BASELINE configs[2]): 4096 keypoint-style instances (n=64, θ=2, unary term), bf16 GEMM /
+    fp32 SDSN, instances split evenly across the ranks (no collective in the data path: "weak" in the
+    per-rank sense is not applicable, the batch is fixed → "strong").  One step = fram_solve_batched
+    over this rank's instances.  `value` = instances solved per second over the job."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2508_00887_b200 as fb
+    from synth import config_c3_batch
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    total = 4096
+    per = total // world
+    insts = config_c3_batch(per, start=rank * per)
+    st = lambda a: torch.tensor(np.ascontiguousarray(np.stack([getattr(i, a) for i in insts])), dtype=torch.float32,
+                                device=dev)
+    A, B, K = st("A"), st("B"), st("K")
+    sch = fb.Schedule(theta=2.0, alpha=SCHEDULE["alpha"], gamma_th=SCHEDULE["gamma_th"], delta_th=SCHEDULE["delta_th"],
+                      max_outer=SCHEDULE["max_outer"], sdsn_max=SCHEDULE["sdsn_max"])
+    h = fb.fram_create(64, lam=SCHEDULE["lam"], schedule=sch, device=local)
+    for _ in range(args.warmup):
+        fb.fram_solve_batched(h, A, B, K, precision=args.precision)
+    sampler = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    tot_ms, res = 0.0, None
+    for _ in range(args.steps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        res = fb.fram_solve_batched(h, A, B, K, precision=args.precision)
+        b.record()
+        b.synchronize()
+        tot_ms += a.elapsed_time(b)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    clocks = sampler.stop()
+    _, stats, X, perm, sts = res
+    perm = perm.cpu().numpy()
+    acc = float(np.mean([(perm[b] == inst.perm_true)[inst.inlier_mask].mean() for b, inst in enumerate(insts)]))
+    if rank == 0:
+        line = {"metric": "FRAM batched instances/s (C3)", "value": total * args.steps / (tot_ms / 1e3),
+                "unit": "instances/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": f"{args.precision}-gemm/f32-sdsn/f64-update",
+                "data": "synthetic (seeded C3 keypoint generator)",
+                "config": {"workload": "C3: 4096 x n=64 keypoint graphs, unary K, theta=2", "batch": total,
+                           "precision": args.precision, "parallelism": f"instances split over {world} rank(s)"},
+                "outer_iters_max": stats["outer_iters"], "total_passes_rank0": stats["total_passes"],
+                "inlier_accuracy_rank0": acc, "gpu_launches": args.steps, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "c5":
         return run_c5(args)
+    if args.workload == "c3":
+        return run_c3(args)
     return run_ours(args)
 
 
