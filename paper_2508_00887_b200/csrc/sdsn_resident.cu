@@ -31,6 +31,7 @@
 #include "common.cuh"
 #include "internal.h"
 #include "tmem_ldst.cuh"
+#include "xchg.cuh"
 
 namespace fram {
 namespace {
@@ -53,83 +54,6 @@ size_t res_smem_bytes(int cpt, int rs, int R) {
   return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 8 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
 }
 
-__device__ __forceinline__ uint64_t tag_f(float v, unsigned e) {
-  return ((uint64_t)e << 32) | __float_as_uint(v);
-}
-__device__ __forceinline__ unsigned tag_of(uint64_t w) { return (unsigned)(w >> 32); }
-__device__ __forceinline__ float val_f(uint64_t w) { return __uint_as_float((unsigned)w); }
-__device__ __forceinline__ uint64_t ld_tag(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_tag(uint64_t* p, uint64_t v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ void st_tag2(uint64_t* p, uint64_t a, uint64_t b) {   // 16-B aligned pair
-  asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
-}
-__device__ __forceinline__ void ld_tag2(const uint64_t* p, uint64_t& a, uint64_t& b) {
-  asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(p) : "memory");
-}
-// an FP64 value published as two tagged words (hi, lo halves)
-__device__ __forceinline__ void st_tag_d(uint64_t* p, double v, unsigned e) {
-  const uint64_t bits = (uint64_t)__double_as_longlong(v);
-  st_tag2(p, ((uint64_t)e << 32) | (bits >> 32), ((uint64_t)e << 32) | (bits & 0xffffffffull));
-}
-__device__ __forceinline__ double wait_tag_d(const uint64_t* p, unsigned e) {
-  uint64_t hi, lo;
-  do { ld_tag2(p, hi, lo); } while (tag_of(hi) != e || tag_of(lo) != e);
-  return __longlong_as_double((long long)(((hi & 0xffffffffull) << 32) | (lo & 0xffffffffull)));
-}
-
-// 32-bit words: a non-negative FP32 magnitude with the epoch parity in the (otherwise zero) sign bit.
-// A slot read for epoch e can only hold epoch e−1 or e (see the ordering argument in the kernel),
-// so one bit distinguishes them.
-__device__ __forceinline__ unsigned ptag(float mag, unsigned e) { return __float_as_uint(mag) | ((e & 1u) << 31); }
-__device__ __forceinline__ bool pok(unsigned w, unsigned e) { return (w >> 31) == (e & 1u); }
-__device__ __forceinline__ float pval(unsigned w) { return __uint_as_float(w & 0x7fffffffu); }
-__device__ __forceinline__ unsigned ld_w(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint4 ld_w4(const unsigned* p) {
-  uint4 v;
-  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_w(unsigned* p, unsigned v) {
-  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_w4(unsigned* p, uint4 v) {
-  asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
-               : "memory");
-}
-// a non-negative FP64 value with a 1-bit tag in the sign bit (one single-copy-atomic 8-byte word)
-__device__ __forceinline__ void st_d1(uint64_t* p, double v, unsigned bit) {
-  const uint64_t w = (uint64_t)__double_as_longlong(v) | ((uint64_t)bit << 63);
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
-}
-__device__ __forceinline__ double wait_d1(const uint64_t* p, unsigned bit) {
-  uint64_t w;
-  do { w = ld_tag(p); } while ((unsigned)(w >> 63) != bit);
-  return __longlong_as_double((long long)(w & 0x7fffffffffffffffull));
-}
-
-// two FP32 adds in one instruction (FADD2, sm_100): d = (a.x + b.x, a.y + b.y), each RN
-__device__ __forceinline__ float2 add2(float2 a, float2 b) {
-  float2 d;
-  asm("{.reg .b64 ra, rb, rd;\n mov.b64 ra, {%2,%3};\n mov.b64 rb, {%4,%5};\n add.rn.f32x2 rd, ra, rb;\n"
-      " mov.b64 {%0,%1}, rd;}"
-      : "=f"(d.x), "=f"(d.y)
-      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
-  return d;
-}
-
-// Threads: warp w → TMEM lane quarter q = w%4, column half h (SPLIT only), row group g.
-// Thread (q, lane, h) owns columns [t·CPT + h·CH, +CH) of every row, t = 32q + lane, CH = CPT/NH.
 template <int CPT> struct RK {
   static constexpr bool SPLIT = CPT >= 8;                // two warps share each TMEM lane's row slice
   static constexpr int NH = SPLIT ? 2 : 1;
