@@ -31,6 +31,9 @@ from .fram_oracle import (  # noqa: F401
     objective_perm,
     matching_error,
     node_accuracy,
+    unary_from_features,
+    pad_attributed,
+    fram_attributed,
 )
 from .lap import lap_max, brute_force_max, perm_score  # noqa: F401
 from .exact import dykstra_project, affine_projection_kkt, qap_brute_force  # noqa: F401

@@ -218,6 +218,48 @@ def fram(A, B, K=None, lam=1.0, theta=10.0, alpha=0.95, gamma_th=1e-3, delta_th=
 
 
 # --------------------------------------------------------------------------------------
+# Attributed graphs of unequal size (NEXT-2 / NEXT-3): K = F F̃ᵀ and padding
+# to a common size with isolated zero-attribute nodes ("n = ñ for simplicity")
+# --------------------------------------------------------------------------------------
+def unary_from_features(F, Ft):
+    """K = F F̃ᵀ  (Eq.(1): ⟨NᵀF, F̃⟩ = ⟨N, F F̃ᵀ⟩; the gradient's unary term λK).
+    F: n1×d, F̃: n2×d → K: n1×n2.  Library matmul as one step."""
+    F = np.asarray(F, np.float64)
+    Ft = np.asarray(Ft, np.float64)
+    if F.ndim != 2 or Ft.ndim != 2 or F.shape[1] != Ft.shape[1]:
+        raise ValueError("F and F̃ must be n1×d and n2×d")
+    return F @ Ft.T
+
+
+def pad_attributed(A, B, F, Ft, m):
+    """Pad G (n1 nodes) and G̃ (n2 nodes) to m ≥ max(n1, n2) nodes by appending isolated nodes with
+    zero attributes (R30): A, Ã → m×m with zero rows/columns, K = F F̃ᵀ → m×m with zero padding."""
+    A = np.asarray(A, np.float64)
+    B = np.asarray(B, np.float64)
+    n1, n2 = A.shape[0], B.shape[0]
+    if m < max(n1, n2):
+        raise ValueError("m must be >= max(n1, n2)")
+    Ap = np.zeros((m, m)); Ap[:n1, :n1] = A
+    Bp = np.zeros((m, m)); Bp[:n2, :n2] = B
+    Kp = None
+    if F is not None:
+        Kp = np.zeros((m, m)); Kp[:n1, :n2] = unary_from_features(F, Ft)
+    return Ap, Bp, Kp
+
+
+def fram_attributed(A, B, F, Ft, m, lam=1.0, **kw):
+    """FRAM on padded attributed graphs (R30): solve the m×m problem, then report, for each of the
+    n1 nodes of G, the matched node of G̃, or −1 when it is matched to a padding node."""
+    n1, n2 = np.asarray(A).shape[0], np.asarray(B).shape[0]
+    Ap, Bp, Kp = pad_attributed(A, B, F, Ft, m)
+    out = fram(Ap, Bp, Kp, lam=lam, **kw)
+    perm = out["perm"][:n1].copy()
+    perm[perm >= n2] = -1
+    out["perm_attr"] = perm
+    return out
+
+
+# --------------------------------------------------------------------------------------
 # Evaluation (Eq.(1) P:65; matching error P:379; accuracy P:383)
 # --------------------------------------------------------------------------------------
 def objective(A, B, K, N, lam=1.0):

@@ -152,3 +152,49 @@ def test_replay_reproduces(rng):
     r1 = oracle.fram(inst.A, inst.B, None, theta=10.0, keep_trace=True)
     r2 = oracle.fram(inst.A, inst.B, None, theta=10.0, replay=r1["passes"], keep_trace=True)
     assert np.array_equal(r1["N"], r2["N"]) and r2["outer_iters"] == r1["outer_iters"]
+
+
+# ---------------------------------------------------------------- attributed / unequal sizes (R30)
+def test_unary_from_features_definition(rng):
+    # K = F F̃ᵀ written out as the feature-term inner product of Eq.(1): ⟨NᵀF, F̃⟩ = ⟨N, K⟩
+    F = rng.random((5, 3))
+    Ft = rng.random((7, 3))
+    K = oracle.unary_from_features(F, Ft)
+    for i in range(5):
+        for j in range(7):
+            assert abs(K[i, j] - sum(F[i, k] * Ft[j, k] for k in range(3))) <= 1e-15
+    N = rng.random((5, 7))
+    assert abs(np.sum((N.T @ F) * Ft) - np.sum(N * K)) <= 1e-12
+
+
+def test_padding_is_inert_for_the_real_nodes(rng):
+    # Isolated zero-attribute padding nodes add nothing to Φ: for any matching of the padded problem,
+    # Φ_padded(M) equals Φ of the original graphs restricted to the real-to-real pairs.
+    n1, n2, m, d = 6, 8, 8, 4
+    A = rng.random((n1, n1)); A = A + A.T
+    B = rng.random((n2, n2)); B = B + B.T
+    F, Ft = rng.random((n1, d)), rng.random((n2, d))
+    Ap, Bp, Kp = oracle.pad_attributed(A, B, F, Ft, m)
+    assert np.all(Ap[n1:] == 0) and np.all(Ap[:, n1:] == 0) and np.all(Kp[n1:] == 0)
+    perm = rng.permutation(m)
+    real = perm[:n1] < n2
+    K = oracle.unary_from_features(F, Ft)
+    pr = perm[:n1]
+    phi = 0.5 * sum(A[i, j] * B[pr[i], pr[j]] for i in range(n1) for j in range(n1) if real[i] and real[j]) + \
+        sum(K[i, pr[i]] for i in range(n1) if real[i])
+    assert abs(oracle.objective_perm(Ap, Bp, Kp, perm) - phi) <= 1e-12
+
+
+def test_fram_attributed_recovers_planted_subgraph():
+    # G is an induced subgraph of G̃ (n1 < n2) with matching nonnegative features (K = FF̃ᵀ ≥ 0, as
+    # the method requires): FRAM on the padded problem recovers the planted embedding (R30).
+    rng = np.random.Generator(np.random.PCG64(77))
+    n2, n1, d = 30, 24, 8
+    B = (rng.random((n2, n2)) < 0.25).astype(float)
+    B = np.triu(B, 1); B = B + B.T
+    Ft = np.maximum(0.0, rng.normal(size=(n2, d)))
+    emb = rng.permutation(n2)[:n1]
+    A = B[np.ix_(emb, emb)]
+    F = Ft[emb]
+    out = oracle.fram_attributed(A, B, F, Ft, n2, lam=1.0, theta=10.0)
+    assert np.array_equal(out["perm_attr"], emb)
