@@ -134,6 +134,20 @@ FRAM_API fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype
                                fram_precision p, void* stream, double* X_out, int32_t* perm_out,
                                int32_t* status_out, fram_stats* stats);
 
+/* Attributed graphs of possibly unequal size (reading R30).
+ *  G has n1 nodes (A: n1×n1, features F: n1×d), G̃ has n2 nodes (B = Ã: n2×n2, F̃: n2×d), all
+ *  row-major contiguous in dtype `dt`, n1, n2 ≤ the handle's n =: m.  Both graphs are padded to m nodes
+ *  with isolated zero-attribute nodes ("n = ñ for simplicity"); the unary term
+ *  K = F·F̃ᵀ (Eq.(1), gradient term λK P:82) is computed on the device in FP64 (DMMA GEMM; zero
+ *  on padding; F, F̃ nullable together ⇒ K = 0) and must be ≥ 0; then Alg. 1 runs as in fram_solve.
+ *  perm_out: int32[n1] — the node of G̃ matched to each node of G, or −1 when it is matched to a padding
+ *  node (n1 > n2).  X_out (nullable): m×m FP64 final N of the padded problem.  Not available on
+ *  sharded handles. */
+FRAM_API fram_status fram_solve_attributed(fram_handle h, fram_dtype dt, int64_t n1, int64_t n2, int64_t d,
+                                  const void* A, const void* B, const void* F, const void* Ft,
+                                  fram_precision p, void* stream, double* X_out, int32_t* perm_out,
+                                  fram_stats* stats);
+
 FRAM_API void fram_destroy(fram_handle h);
 
 /* Thread-local message for the last non-OK status on this thread ("" if none). */

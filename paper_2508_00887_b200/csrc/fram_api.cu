@@ -61,7 +61,8 @@ struct fram_ctx {
   // workspace
   DevBuf Aq, BqT, Kq, N, Nq, UT, Y, colpart, Spart, Mpart, cvec, bar, scal, ghist, upd, lapw, permd;
   DevBuf rcolpart, rbvec, rflags, rdbg;
-  DevBuf shUT, shUblk, shRsum, shSend, shRecv, shState, shNfull, shColpart, shScan;   // sharded solve   // on-chip-resident SDSN (K4r)
+  DevBuf shUT, shUblk, shRsum, shSend, shRecv, shState, shNfull, shColpart, shScan;   // sharded solve
+  DevBuf atA, atB, atK, atF, atFt, atPerm;                                           // attributed solve   // on-chip-resident SDSN (K4r)
   DevBuf stA, stB, stK, stX0, stX;
   DevBuf scan;
   double* hscal = nullptr;          // pinned readback
@@ -547,7 +548,8 @@ void fram_destroy(fram_handle h) {
   DevBuf* bufs[] = {&h->Aq, &h->BqT, &h->Kq, &h->N, &h->Nq, &h->UT, &h->Y, &h->colpart, &h->Spart, &h->Mpart,
                     &h->cvec, &h->bar, &h->scal, &h->ghist, &h->upd, &h->lapw, &h->permd, &h->stA, &h->stB,
                     &h->stK, &h->stX0, &h->stX, &h->scan, &h->rcolpart, &h->rbvec, &h->rflags, &h->rdbg, &h->shUT, &h->shUblk, &h->shRsum,
-                    &h->shSend, &h->shRecv, &h->shState, &h->shNfull, &h->shColpart, &h->shScan};
+                    &h->shSend, &h->shRecv, &h->shState, &h->shNfull, &h->shColpart, &h->shScan, &h->atA,
+                    &h->atB, &h->atK, &h->atF, &h->atFt, &h->atPerm};
   for (DevBuf* b : bufs) b->release();
   if (h->hscal) cudaFreeHost(h->hscal);
   for (auto& e : h->ev)
@@ -772,6 +774,62 @@ fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype dt, cons
                                       h->num_sms, &err);
   if (s != FRAM_OK) g_err = err;
   return s;
+}
+
+fram_status fram_solve_attributed(fram_handle h, fram_dtype dt, int64_t n1, int64_t n2, int64_t d, const void* A,
+                                  const void* B, const void* F, const void* Ft, fram_precision p, void* stream,
+                                  double* X_out, int32_t* perm_out, fram_stats* stats) {
+  fram_status s0 = common_checks(h, (int)dt, p);
+  if (s0 != FRAM_OK) return s0;
+  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  const long m = h->n;
+  if (!A || !B || n1 < 1 || n2 < 1 || n1 > m || n2 > m) return fail(FRAM_ERR_USAGE, "need 1 <= n1, n2 <= handle n");
+  if ((F == nullptr) != (Ft == nullptr) || (F && d < 1)) return fail(FRAM_ERR_USAGE, "F and Ft go together, d >= 1");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const size_t es = dt_size((int)dt);
+  fram_status rs;
+  const void *dA, *dB, *dF = nullptr, *dFt = nullptr;
+  if ((rs = stage_in(h, h->stA, A, (size_t)n1 * n1 * es, st, &dA)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stB, B, (size_t)n2 * n2 * es, st, &dB)) != FRAM_OK) return rs;
+  if (F) {
+    if ((rs = stage_in(h, h->atF, F, (size_t)n1 * d * es, st, &dF)) != FRAM_OK) return rs;
+    if ((rs = stage_in(h, h->atFt, Ft, (size_t)n2 * d * es, st, &dFt)) != FRAM_OK) return rs;
+  }
+  // R30: pad A, Ã to m×m (FP64) with isolated zero-attribute nodes; K = F F̃ᵀ in FP64, zero on padding
+  CK(h->atA.ensure((size_t)m * m * 8), "alloc padded A");
+  CK(h->atB.ensure((size_t)m * m * 8), "alloc padded B");
+  CK(fram::launch_pad_convert(h->atA.as<double>(), m, m, m, dA, (int)dt, n1, n1, n1, st), "pad A");
+  CK(fram::launch_pad_convert(h->atB.as<double>(), m, m, m, dB, (int)dt, n2, n2, n2, st), "pad B");
+  h->launches += 2;
+  const double* dK = nullptr;
+  if (F) {
+    const long ldd = (d + 1) / 2 * 2;                          // 16-byte rows for the DMMA loader
+    CK(h->stX.ensure((size_t)2 * m * ldd * 8), "alloc features");
+    double* Fq = h->stX.as<double>();
+    double* Ftq = Fq + (size_t)m * ldd;
+    CK(fram::launch_pad_convert(Fq, ldd, m, ldd, dF, (int)dt, d, n1, d, st), "pad F");
+    CK(fram::launch_pad_convert(Ftq, ldd, m, ldd, dFt, (int)dt, d, n2, d, st), "pad Ft");
+    CK(h->atK.ensure((size_t)m * m * 8), "alloc K");
+    fram::GemmArgs gk{Fq, Ftq, m, m, d, ldd, 1, h->atK.p, m, nullptr, 0.0};   // K = F·F̃ᵀ (NT, FP64)
+    CK(fram::launch_gemm_f64(gk, st), "K = F Ft^T");
+    h->launches += 3;
+    dK = h->atK.as<double>();
+  }
+  CK(h->atPerm.ensure((size_t)m * 4), "alloc perm");
+  const int64_t launches_before = h->launches;
+  fram_status so = fram_solve(h, FRAM_DT_F64, h->atA.p, h->atB.p, dK, nullptr, p, stream, X_out,
+                              h->atPerm.as<int32_t>(), stats);
+  if (so != FRAM_OK && so != FRAM_NOT_CONVERGED) return so;
+  if (stats) stats->kernel_launches += launches_before;
+  if (perm_out) {
+    std::vector<int32_t> pm((size_t)m);
+    CK(cudaMemcpy(pm.data(), h->atPerm.p, (size_t)m * 4, cudaMemcpyDeviceToHost), "perm readback");
+    std::vector<int32_t> out((size_t)n1);
+    for (long i = 0; i < n1; ++i) out[i] = pm[i] < n2 ? pm[i] : -1;
+    CK(cudaMemcpyAsync(perm_out, out.data(), (size_t)n1 * 4, cudaMemcpyDefault, st), "perm copy");
+    CK(cudaStreamSynchronize(st), "perm sync");
+  }
+  return so;
 }
 
 fram_status fram_get_unique_id(uint8_t id[128]) {

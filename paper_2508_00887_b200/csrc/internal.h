@@ -123,6 +123,8 @@ cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* wo
 size_t lap_work_bytes(long n);
 
 // ---- misc ---------------------------------------------------------------------------------------
+cudaError_t launch_pad_convert(double* dst, long ldd, long drows, long dcols, const void* src, int dt, long lds,
+                               long rows, long cols, cudaStream_t st);
 cudaError_t launch_copy2d_f64(double* dst, long ldd, const double* src, long lds, long rows,
                               long cols, cudaStream_t st);
 cudaError_t launch_scan_nonneg(const void* X, bool f64, long n, unsigned long long* bad,

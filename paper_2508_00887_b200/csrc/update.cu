@@ -82,6 +82,23 @@ __global__ void init_n_kernel(double* N, void* Nq, const double* X0, long rows, 
     }
 }
 
+// dst (drows × dcols, leading dim ldd, FP64) ← src (rows × cols of dtype dt, leading dim lds), zero
+// outside the source block (padding of attributed graphs, R30)
+__global__ void pad_convert_kernel(double* dst, long ldd, long drows, long dcols, const void* src, int dt, long lds,
+                                   long rows, long cols) {
+  for (long i = blockIdx.x; i < drows; i += gridDim.x)
+    for (long j = threadIdx.x; j < dcols; j += blockDim.x) {
+      double v = 0.0;
+      if (i < rows && j < cols) {
+        const long idx = i * lds + j;
+        if (dt == 0) v = reinterpret_cast<const double*>(src)[idx];
+        else if (dt == 1) v = (double)reinterpret_cast<const float*>(src)[idx];
+        else v = (double)__bfloat162float(reinterpret_cast<const __nv_bfloat16*>(src)[idx]);
+      }
+      dst[i * ldd + j] = v;
+    }
+}
+
 __global__ void copy2d_kernel(double* dst, long ldd, const double* src, long lds, long rows, long cols) {
   for (long i = blockIdx.x; i < rows; i += gridDim.x)
     for (long j = threadIdx.x; j < cols; j += blockDim.x) dst[i * ldd + j] = src[i * lds + j];
@@ -119,6 +136,13 @@ cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long ro
     case 3: init_n_kernel<3><<<grid, 256, 0, st>>>(N, Nq, X0, rows, n, ld); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_convert(double* dst, long ldd, long drows, long dcols, const void* src, int dt, long lds,
+                               long rows, long cols, cudaStream_t st) {
+  const int grid = (int)(drows < 2048 ? drows : 2048);
+  pad_convert_kernel<<<grid < 1 ? 1 : grid, 256, 0, st>>>(dst, ldd, drows, dcols, src, dt, lds, rows, cols);
   return cudaGetLastError();
 }
 

@@ -24,7 +24,7 @@ FLAG_TRACE, FLAG_CHECK_SYMMETRY, FLAG_NO_THETA_SCALE, FLAG_TIME_PHASES = 1, 2, 4
 
 EXPORTED = ["fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_destroy",
             "fram_last_error", "fram_get_unique_id", "fram_create_sharded", "fram_sdsn", "fram_gradient",
-            "fram_lap", "fram_abi_version", "fram_build_info"]
+            "fram_lap", "fram_abi_version", "fram_build_info", "fram_solve_attributed"]
 
 
 class FramError(RuntimeError):
@@ -99,7 +99,10 @@ def lib():
     L.fram_gradient.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, C.POINTER(dbl)]
     L.fram_lap.argtypes = [vp, vp, vp, vp]
     L.fram_build_info.restype = C.c_char_p
+    L.fram_solve_attributed.argtypes = [vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, vp, vp, vp, vp, C.c_int, vp, vp,
+                                        vp, C.POINTER(_Stats)]
     for f in ("fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_get_unique_id",
+              "fram_solve_attributed",
               "fram_create_sharded", "fram_sdsn", "fram_gradient", "fram_lap"):
         getattr(L, f).restype = C.c_int
     _lib_handle = L
@@ -223,6 +226,28 @@ def fram_solve(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, 
     st.gamma_last = C.cast(arrays[2], C.POINTER(C.c_double))
     status = lib().fram_solve(h.ptr, _dt_of(A), _ptr(A), _ptr(B), _ptr(K), _ptr(X0), PREC[precision],
                               _stream(stream, A), _ptr(X_out), _ptr(perm_out), C.byref(st))
+    _check(status, allow_nc=True)
+    return status, _stats_dict(st, n, arrays), X_out, perm_out
+
+
+def fram_solve_attributed(h: Handle, A, B, F=None, Ft=None, precision="bf16", stream=None, X_out=None,
+                          perm_out=None, max_outer=1000):
+    """Attributed graphs of possibly unequal size (R30): A n1×n1, B n2×n2, F n1×d, F̃ n2×d; padded to
+    the handle's n; K = F F̃ᵀ on the device.  Returns (status, stats, X_out (n×n), perm_out (n1; −1 =
+    matched to a padding node))."""
+    n = h.n
+    n1, n2 = A.shape[0], B.shape[0]
+    d = 0 if F is None else F.shape[1]
+    X_out = _like(A, (n, n), "f64") if X_out is None else X_out
+    perm_out = _like(A, (n1,), "i32") if perm_out is None else perm_out
+    arrays = ((C.c_int32 * max_outer)(), (C.c_double * max_outer)(), (C.c_double * max_outer)())
+    st = _Stats()
+    st.passes_per_iter = C.cast(arrays[0], C.POINTER(C.c_int32))
+    st.delta_trace = C.cast(arrays[1], C.POINTER(C.c_double))
+    st.gamma_last = C.cast(arrays[2], C.POINTER(C.c_double))
+    status = lib().fram_solve_attributed(h.ptr, _dt_of(A), int(n1), int(n2), int(d), _ptr(A), _ptr(B), _ptr(F),
+                                         _ptr(Ft), PREC[precision], _stream(stream, A), _ptr(X_out),
+                                         _ptr(perm_out), C.byref(st))
     _check(status, allow_nc=True)
     return status, _stats_dict(st, n, arrays), X_out, perm_out
 
