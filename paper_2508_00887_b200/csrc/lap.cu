@@ -89,27 +89,40 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
     int j0 = 0, i0 = i;
     load_row(i0);
     while (true) {
-      // used[j0] = true (the owner remembers p[j0] = i0 for the potential updates)
+      // used[j0] = true (the owner remembers p[j0] = i0 for the potential updates).  A used column's
+      // minv is never read again in this search (oracle: only free columns are scanned and updated),
+      // so it is parked at +inf: the scan and the `minv −= δ` update then need no free-column mask.
       if (j0 > 0 && ((j0 - 1) % THREADS) == tid) {
         const int kk = (j0 - 1) / THREADS;
         fr &= ~(one << kk);
 #pragma unroll
-        for (int k = 0; k < CPT; ++k) prow[k] = (k == kk) ? i0 : prow[k];
+        for (int k = 0; k < CPT; ++k) {
+          prow[k] = (k == kk) ? i0 : prow[k];
+          minv[k] = (k == kk) ? CUDART_INF : minv[k];
+        }
       }
       const double ui0 = u[i0];                       // not written during this step (i0 ∉ tree)
-      double best = CUDART_INF;
-      int bj = 0x7fffffff;
+      double bv[CPT];
 #pragma unroll
-      for (int k = 0; k < CPT; ++k) {                 // k ascending ⇒ j ascending: strict < keeps lowest j
+      for (int k = 0; k < CPT; ++k) {
         const bool f = (fr >> k) & one;
         const double cur = __dsub_rn(__dsub_rn(-cv[k], ui0), v[k]);     // (C[i0][j] − u[i0]) − v[j]
         const bool upd = f && cur < minv[k];
         minv[k] = upd ? cur : minv[k];
         if (upd) way[1 + tid + k * THREADS] = j0;
-        const bool bt = f && minv[k] < best;
-        best = bt ? minv[k] : best;
-        bj = bt ? 1 + tid + k * THREADS : bj;
+        bv[k] = minv[k];                              // +inf for used / absent columns
       }
+      // thread-local argmin as a tree over k (j ascending with k: strict < keeps the lower j)
+      int bk[CPT];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k) bk[k] = k;
+#pragma unroll
+      for (int w = 1; w < CPT; w *= 2)
+#pragma unroll
+        for (int k = 0; k + w < CPT; k += 2 * w)
+          if (bv[k + w] < bv[k]) { bv[k] = bv[k + w]; bk[k] = bk[k + w]; }
+      const double best = bv[0];
+      int bj = best < CUDART_INF ? 1 + tid + bk[0] * THREADS : 0x7fffffff;
       uint64_t key = okey(best);
       warp_argmin(key, bj);
       if (lane == 0) { s_k[par][warp] = key; s_j[par][warp] = bj; }
@@ -130,7 +143,7 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
           u[prow[k]] = __dadd_rn(u[prow[k]], delta);
           v[k] = __dsub_rn(v[k], delta);
         }
-        minv[k] = ((fr >> k) & one) ? __dsub_rn(minv[k], delta) : minv[k];
+        minv[k] = __dsub_rn(minv[k], delta);         // free: as the oracle; used/absent: +inf stays +inf
       }
       if (tid == 0) u[i] = __dadd_rn(u[i], delta);
       j0 = j1;
