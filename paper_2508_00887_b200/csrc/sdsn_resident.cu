@@ -258,15 +258,15 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   // this warp's partials of rows ra and rb (rb < 0: none): two interleaved shuffle trees, lane 0
   // stores them at slot 4·h + q of the row (fixed order, deterministic)
   auto put_rowparts = [&](int ra, float va, int rb, float vb) {
+    // transpose-reduce: one xor-16 exchange leaves lanes 0-15 with row a and lanes 16-31 with row b,
+    // four more levels finish both (5 shuffles for two rows instead of 10); fixed tree, deterministic
+    const bool lo = lane < 16;
+    float keep = lo ? va : vb;
+    keep += __shfl_xor_sync(0xffffffffu, lo ? vb : va, 16);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      va += __shfl_xor_sync(0xffffffffu, va, o);
-      vb += __shfl_xor_sync(0xffffffffu, vb, o);
-    }
-    if (lane == 0) {
-      s_rowpart[ra * 8 + 4 * h + q] = va;
-      if (rb >= 0) s_rowpart[rb * 8 + 4 * h + q] = vb;
-    }
+    for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+    if (lane == 0) s_rowpart[ra * 8 + 4 * h + q] = keep;
+    if (lane == 16 && rb >= 0) s_rowpart[rb * 8 + 4 * h + q] = keep;
   };
 
   // Y0 = fl(s·X) (Alg.2 step 1; skipped when !P.scale) with its sums
