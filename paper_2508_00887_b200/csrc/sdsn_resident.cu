@@ -395,14 +395,15 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       }
       __syncthreads();
     }
-    if (warp == 1) {                                     // S of epoch e (row-sum partials, parity buffer)
-      double sacc = 0.0;
+  };
+  // S of epoch e (row-sum partials, parity buffer), waited for by one warp while the others wait for b
+  auto wait_S = [&](unsigned e) {
+    double sacc = 0.0;
 #pragma unroll
-      for (int i = 0; i < kResKMax; ++i)
-        if (lane + 32 * i < G) sacc += wait_d1(P.Spart + (size_t)(e & 1) * G + lane + 32 * i, (e >> 1) & 1u);
-      sacc = warp_sum_d(sacc);
-      if (lane == 0) s_S = sacc;
-    }
+    for (int i = 0; i < kResKMax; ++i)
+      if (lane + 32 * i < G) sacc += wait_d1(P.Spart + (size_t)(e & 1) * G + lane + 32 * i, (e >> 1) & 1u);
+    sacc = warp_sum_d(sacc);
+    if (lane == 0) s_S = sacc;
   };
 
   // ---------------- phase S: Y0 = s·X (on chip) and its sums ----------------
@@ -424,18 +425,13 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   };
   for (;; ++j) {
     long long t0 = now();
-    const double S = s_S;                               // written by warp 1 in slice(ep), synced
-    gam = S / dn - 1.0;                                                 // γ_j (P:282)
-    if (b == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[j] = gam;
-    const bool last = P.sdsn_fixed > 0 ? (j + 1 >= P.sdsn_fixed)
-                                       : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
-    const double abase = 1.0 / dn + S / nn;
-    for (int i = tid; i < R; i += THREADS) s_a[i] = (float)(abase - s_r[i] / dn);
+    // pass boundary: every thread waits for its b values of epoch ep while warp 1 also collects S
     float2 bv[CH / 2];                                   // b_j pairs (register pairs for FADD2)
     {
       uint4 w[VH];
 #pragma unroll
       for (int c = 0; c < VH; ++c) w[c] = ld_w4(P.bvec + (size_t)((c0 + c) * 128 + t) * 4);
+      if (warp == 1) wait_S(ep);
       bool ok;
       do {                                               // wait for every b of epoch ep
         ok = true;
@@ -453,6 +449,14 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
         bv[2 * c + 1] = make_float2(-pval(w[c].z), -pval(w[c].w));
       }
     }
+    __syncthreads();
+    const double S = s_S;                               // written by warp 1 (wait_S), synced
+    gam = S / dn - 1.0;                                                 // γ_j (P:282)
+    if (b == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[j] = gam;
+    const bool last = P.sdsn_fixed > 0 ? (j + 1 >= P.sdsn_fixed)
+                                       : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
+    const double abase = 1.0 / dn + S / nn;
+    for (int i = tid; i < R; i += THREADS) s_a[i] = (float)(abase - s_r[i] / dn);
     __syncthreads();
     long long t1 = now();
     sweep_pass(bv, last ? 0u : ep + 1);
