@@ -257,8 +257,6 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
     r.gamma_hist = h->ghist.as<double>();
     r.sdsn_out = scal;
     static const bool timing = getenv("FRAM_RES_TIMING") != nullptr;
-    static const int dbgmode = getenv("FRAM_RES_DBGMODE") ? atoi(getenv("FRAM_RES_DBGMODE")) : 0;
-    r.dbgmode = dbgmode;
     if (timing) {
       CK(h->rdbg.ensure((size_t)h->num_sms * 8 * 8), "alloc dbg");
       r.dbg = h->rdbg.as<long long>();

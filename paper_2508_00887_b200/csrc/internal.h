@@ -19,7 +19,6 @@ struct SdsnParams {
   int* passes_out;     // [1]
   double* gamma_hist;  // [sdsn_max] nullable: γ_j of every pass input
   double* sdsn_out;    // [4]: [0] γ of the last pass input, [1] max X, [2] S of last input
-  int debug;           // dev-only timing knobs (FRAM_SDSN_DEBUG): 1 skip sweeps, 2 skip barriers/reductions
 };
 // f64: T=double; else T=float.  Returns the grid used via *grid_out.
 cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_sms, int* grid_out);
@@ -43,7 +42,6 @@ struct ResParams {
   int rs;              // rows per CTA held in shared memory (set by the launcher)
   int rmax;            // rows per CTA upper bound (set by the launcher)
   long long* dbg;      // dev-only (FRAM_RES_TIMING): per-CTA phase times [grid][8], nullable
-  int dbgmode;         // dev-only (FRAM_RES_DBGMODE): 1 skip SMEM rows, 2 skip TMEM rows (timing only)
 };
 int sdsn_res_grid(long n, int num_sms);       // 0 ⇒ n not supported on chip
 long sdsn_res_slots(long n);

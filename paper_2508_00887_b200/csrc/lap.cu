@@ -187,12 +187,7 @@ cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* wo
   if (n <= 512) return launch_t<512, 1>(N, n, ld, perm, work, st);
   if (n <= 1024) return launch_t<512, 2>(N, n, ld, perm, work, st);
   if (n <= 2048) return launch_t<512, 4>(N, n, ld, perm, work, st);
-  if (n <= 4096) {
-    static const int cfg = getenv("FRAM_LAP_CFG") ? atoi(getenv("FRAM_LAP_CFG")) : 512;   // dev knob
-    if (cfg == 256) return launch_t<256, 16>(N, n, ld, perm, work, st);
-    if (cfg == 1024) return launch_t<1024, 4>(N, n, ld, perm, work, st);
-    return launch_t<512, 8>(N, n, ld, perm, work, st);
-  }
+  if (n <= 4096) return launch_t<512, 8>(N, n, ld, perm, work, st);   // measured best of 256/512/1024 threads
   if (n <= 8192) return launch_t<1024, 8>(N, n, ld, perm, work, st);
   if (n <= 16384) return launch_t<1024, 16>(N, n, ld, perm, work, st);
   if (n <= 65536) return launch_t<1024, 64>(N, n, ld, perm, work, st);

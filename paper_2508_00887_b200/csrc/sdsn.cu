@@ -309,9 +309,8 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
         bv[k][w] = (q * W + w < n) ? (T)(-ldcg(P.cvec + q * W + w) / dn) : (T)0;
     }
     __syncthreads();
-    if (!(P.debug & 1)) sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv);
+    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv);
     if (last) break;
-    if (P.debug & 2) { __syncthreads(); continue; }
     grid_barrier(P.bar, G);
     reduce_columns_and_S();
     grid_barrier(P.bar, G);
@@ -361,7 +360,6 @@ static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int 
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   if (e != cudaSuccess) return e;
   SdsnParams pp = p;
-  if (const char* dbg = getenv("FRAM_SDSN_DEBUG")) pp.debug = atoi(dbg);
   int cgv = cg;
   void* args[] = {&pp, &cgv};
   return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kSdsnThreads), args, dsm, st);

@@ -319,8 +319,6 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     int rbeg, rend, rstep;
     if (R > RT) { rbeg = g == 0 ? 0 : RT; rend = g == 0 ? RT : R; rstep = 1; }
     else { rbeg = g; rend = R; rstep = 2; }
-    if (P.dbgmode & 1) rend = min(rend, RT);           // dev timing knobs (FRAM_RES_DBGMODE)
-    if ((P.dbgmode & 2) && rbeg < RT) rbeg = rend;
     int ra = rbeg;
     for (; ra + rstep < rend; ra += 2 * rstep) {         // two rows at a time
       const int rb = ra + rstep;
@@ -512,15 +510,6 @@ int cpt_for(long n) {
   return 0;
 }
 
-int rows_target() {
-  static int rt = -1;
-  if (rt < 0) {
-    const char* e = getenv("FRAM_RES_ROWS");
-    rt = e ? atoi(e) : 16;
-    if (rt < 1) rt = 16;
-  }
-  return rt;
-}
 
 template <int CPT>
 cudaError_t launch_res_t(ResParams p, cudaStream_t st, int G) {
@@ -554,7 +543,7 @@ cudaError_t launch_res_t(ResParams p, cudaStream_t st, int G) {
 int sdsn_res_grid(long n, int num_sms) {
   const int cpt = cpt_for(n);
   if (cpt == 0) return 0;
-  long G = (n + rows_target() - 1) / rows_target();
+  long G = (n + 15) / 16;                               // ~16 rows per CTA, more CTAs if needed
   if (G > num_sms) G = num_sms;
   if (G < 1) G = 1;
   auto R_of = [&](long G_) { return (int)((n + G_ - 1) / G_); };
