@@ -66,7 +66,7 @@ struct ShardSdsnParams {
   ShardSdsnState* state;
 };
 int sdsn_sh_grid(long rows, int num_sms, bool f64);
-size_t sdsn_sh_smem(long ld, bool f64);
+size_t sdsn_sh_smem(long ld, bool f64, long rows_max);
 cudaError_t launch_sdsn_sh_max(const ShardSdsnParams& p, bool f64, cudaStream_t st, int num_sms);
 // mode 0: scale sweep (after the max all-reduce), mode 1: pass `pass`; both end with the local
 // column/mass reduction into p.send (the caller all-reduces send → recv)

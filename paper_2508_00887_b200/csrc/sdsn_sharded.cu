@@ -104,44 +104,58 @@ __global__ void __launch_bounds__(kShThreads) sh_pass_kernel(ShardSdsnParams P, 
     }
   }
   __syncthreads();
+  // row partials per warp in shared memory (no barrier per row); combined once after the sweep
+  double* s_rp = reinterpret_cast<double*>(BS ? s_b + ld : s_col + ld);   // [rows of this CTA][warps]
   for (long i = r0; i < r1; ++i) {
     VT* row = reinterpret_cast<VT*>(Y + i * ld);
     const T a = mode ? (T)(abase - P.rsum[i] / dn) : (T)0;      // R9: a_i in FP64, rounded
     double rs = 0.0;
-    for (long q = tid; q < nvec; q += kShThreads) {
-      T e[W], c[W], bb[W];
-      vsplit<T>(row[q], e);
-      vsplit<T>(reinterpret_cast<VT*>(s_col)[q], c);
-      if (BS && mode) vsplit<T>(reinterpret_cast<VT*>(s_b)[q], bb);
-      T rp = (T)0;
+    constexpr int NB = 8;                                        // vectors per thread loaded together
+    for (long q0 = tid; q0 < nvec; q0 += (long)NB * kShThreads) {
+      VT ev[NB];
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const long j = q * W + w;
-        T y;
-        if (j >= n) y = (T)0;
-        else if (mode) {                                         // P2(P1(Y)), R9 grouping
-          const T bj = BS ? bb[w] : (T)(-P.recv[j] / dn);
-          y = (e[w] + a) + bj;
-          y = y > (T)0 ? y : (T)0;
-        }
-        else y = P.scale ? (T)(sc * (double)e[w]) : e[w];
-        e[w] = y;
-        c[w] += y;
-        rp += y;
+      for (int u = 0; u < NB; ++u) {                             // all loads first (memory-level parallelism)
+        const long q = q0 + (long)u * kShThreads;
+        if (q < nvec) ev[u] = row[q];
       }
-      row[q] = vjoin<T>(e);
-      reinterpret_cast<VT*>(s_col)[q] = vjoin<T>(c);
-      rs += (double)rp;
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const long q = q0 + (long)u * kShThreads;
+        if (q >= nvec) break;
+        T e[W], c[W], bb[W];
+        vsplit<T>(ev[u], e);
+        vsplit<T>(reinterpret_cast<VT*>(s_col)[q], c);
+        if (BS && mode) vsplit<T>(reinterpret_cast<VT*>(s_b)[q], bb);
+        T rp = (T)0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const long j = q * W + w;
+          T y;
+          if (j >= n) y = (T)0;
+          else if (mode) {                                       // P2(P1(Y)), R9 grouping
+            const T bj = BS ? bb[w] : (T)(-P.recv[j] / dn);
+            y = (e[w] + a) + bj;
+            y = y > (T)0 ? y : (T)0;
+          }
+          else y = P.scale ? (T)(sc * (double)e[w]) : e[w];
+          e[w] = y;
+          c[w] += y;
+          rp += y;
+        }
+        row[q] = vjoin<T>(e);
+        reinterpret_cast<VT*>(s_col)[q] = vjoin<T>(c);
+        rs += (double)rp;
+      }
     }
     rs = warp_sum_d(rs);
-    if (lane == 0) s_w[warp] = rs;
-    __syncthreads();
-    if (tid == 0) {
-      double r = 0.0;
-      for (int w = 0; w < kShThreads / 32; ++w) r += s_w[w];
-      P.rsum[i] = r;
-    }
-    __syncthreads();
+    if (lane == 0) s_rp[(i - r0) * (kShThreads / 32) + warp] = rs;
+  }
+  __syncthreads();
+  for (long i = r0 + tid; i < r1; i += kShThreads) {             // fixed order over warps
+    double r = 0.0;
+#pragma unroll
+    for (int w = 0; w < kShThreads / 32; ++w) r += s_rp[(i - r0) * (kShThreads / 32) + w];
+    P.rsum[i] = r;
   }
   T* dst = reinterpret_cast<T*>(P.colpart) + (long)blockIdx.x * ld;
   for (long q = tid; q < nvec; q += kShThreads) reinterpret_cast<VT*>(dst)[q] = reinterpret_cast<VT*>(s_col)[q];
@@ -191,7 +205,10 @@ int sdsn_sh_grid(long rows, int num_sms, bool f64) {
   return (int)(g < 1 ? 1 : g);
 }
 
-size_t sdsn_sh_smem(long ld, bool f64) { return (size_t)ld * (f64 ? 8 : 8); }   // FP32: partials + b
+// column partials + b (FP32 mode) + per-warp row partials of up to rows_max rows
+size_t sdsn_sh_smem(long ld, bool f64, long rows_max) {
+  return (size_t)ld * (f64 ? 8 : 8) + (size_t)rows_max * (kShThreads / 32) * 8;
+}
 
 cudaError_t launch_sdsn_sh_max(const ShardSdsnParams& p, bool f64, cudaStream_t st, int num_sms) {
   cudaError_t e = cudaMemsetAsync(p.send, 0, sizeof(double), st);
@@ -204,7 +221,7 @@ cudaError_t launch_sdsn_sh_max(const ShardSdsnParams& p, bool f64, cudaStream_t 
 
 cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, int pass, cudaStream_t st, int num_sms) {
   const int g = sdsn_sh_grid(p.rows, num_sms, f64);
-  const size_t sm = sdsn_sh_smem(p.ld, f64);
+  const size_t sm = sdsn_sh_smem(p.ld, f64, (p.rows + g - 1) / g + 1);
   if (f64) {
     cudaError_t e = cudaFuncSetAttribute(sh_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
