@@ -292,7 +292,8 @@ def run_ours(args):
     resident = stats[0].get("sdsn_kernel", 1) == 2
     avg_launch_s = ms_sdsn / 1e3 / sdsn_launches
     passes_per_launch = passes / sdsn_launches
-    bytes_per_launch = 8.0 * n * n * passes_per_launch       # algorithmic: FP32 Y read + write per pass
+    esz = 8.0 if args.precision == "fp64" else 4.0            # SDSN iterate: FP64 in FP64 mode, else FP32
+    bytes_per_launch = 2.0 * esz * n * n * passes_per_launch  # algorithmic: Y read + write per pass
     hbm_equiv = bytes_per_launch / avg_launch_s / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "sdsn_traffic.json")
@@ -321,7 +322,8 @@ def run_ours(args):
                 "hbm_equivalent": {"achieved_gbs": hbm_equiv, "peak_gbs": hbm, "frac": hbm_equiv / hbm,
                                    "note": "algorithmic 8n^2 B/pass over the launch time; the iterate never leaves the chip"}}
     else:
-        roof = {"kernel": "sdsn_kernel<float> (K4, streaming through L2/HBM)", "bound": "hbm", "achieved": hbm_equiv,
+        roof = {"kernel": f"sdsn_kernel<{'double' if esz == 8 else 'float'}> (K4, streaming through L2/HBM)",
+                "bound": "hbm", "achieved": hbm_equiv,
                 "peak": hbm, "unit": "GB/s", "frac": hbm_equiv / hbm, "traffic": traffic, "peak_source": psrc,
                 "algorithmic_bytes_per_launch": bytes_per_launch}
     roof.update({"passes_per_launch": passes_per_launch, "ms_per_launch": avg_launch_s * 1e3,
