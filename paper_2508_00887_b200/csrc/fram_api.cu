@@ -258,23 +258,38 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
     r.sdsn_out = scal;
     static const bool timing = getenv("FRAM_RES_TIMING") != nullptr;
     if (timing) {
-      CK(h->rdbg.ensure((size_t)h->num_sms * 8 * 8), "alloc dbg");
+      CK(h->rdbg.ensure((size_t)h->num_sms * 24 * 8), "alloc dbg");
       r.dbg = h->rdbg.as<long long>();
+      CK(cudaMemsetAsync(r.dbg, 0, (size_t)h->num_sms * 24 * 8, st), "dbg memset");
     }
     CK(fram::launch_sdsn_resident(r, st, h->num_sms), "sdsn (on-chip) launch");
     if (timing) {
-      std::vector<long long> d((size_t)h->num_sms * 8);
+      std::vector<long long> d((size_t)h->num_sms * 24);
       CK(cudaMemcpyAsync(d.data(), r.dbg, d.size() * 8, cudaMemcpyDeviceToHost, st), "dbg");
       CK(cudaStreamSynchronize(st), "dbg sync");
       const int G = fram::sdsn_res_grid(h->n, h->num_sms);
       double mx[6] = {0};
       for (int bb = 0; bb < G; ++bb)
-        for (int k = 0; k < 6; ++k) mx[k] = std::max(mx[k], (double)d[bb * 8 + k]);
+        for (int k = 0; k < 6; ++k) mx[k] = std::max(mx[k], (double)d[bb * 16 + k]);
       const double np = std::max(1.0, (double)(d[5] & 0xffff));
       fprintf(stderr, "[res timing] CTA0 load phase %.1f us, kernel start→loop end %.1f us\n", (d[5] >> 16) / 1e3, d[3] / 1e3);
-      fprintf(stderr, "[res timing n=%ld G=%d passes=%.0f] ns/pass (CTA0): bload %.0f sweep %.0f [spart %.0f stores %.0f srows %.0f sync %.0f] slice %.0f | max over CTAs: %.0f %.0f %.0f\n",
-              (long)h->n, G, np, d[0] / np, d[1] / np, d[2] / np, d[4] / np, d[6] / np, d[7] / np, 0.0, mx[0] / np, mx[1] / np,
-              0.0);
+      fprintf(stderr, "[res timing n=%ld G=%d passes=%.0f] ns/pass (CTA0): bload %.0f sweep %.0f [rows g0 %.0f g1 %.0f; spart %.0f stores %.0f srows %.0f sync %.0f] slice %.0f | max over CTAs: %.0f %.0f\n",
+              (long)h->n, G, np, d[0] / np, d[1] / np, d[9] / np, d[10] / np, d[2] / np, d[4] / np, d[6] / np, d[7] / np,
+              d[8] / np, mx[0] / np, mx[1] / np);
+      {   // timeline of pass 500: per stamp, min / median / max over CTAs relative to the earliest pass start
+        const long long* tl = d.data() + (size_t)G * 16;
+        long long base = tl[0];
+        for (int bb = 0; bb < G; ++bb) base = std::min(base, tl[bb * 8]);
+        const char* names[6] = {"pass start", "b ready (g0)", "after sync", "sweep+epilogue end", "slice polls done", "slice end"};
+        for (int k = 0; k < 6 && base > 0; ++k) {
+          std::vector<long long> v;
+          for (int bb = 0; bb < G; ++bb) v.push_back(tl[bb * 8 + k] - base);
+          std::sort(v.begin(), v.end());
+          fprintf(stderr, "[res timeline p500] %-20s min %6lld med %6lld max %6lld ns\n", names[k], v.front(), v[v.size() / 2], v.back());
+        }
+      }
+      fprintf(stderr, "[res timing] rows cycles/pass g0 %.0f g1 %.0f -> SM clock %.0f / %.0f MHz\n", d[11] / np, d[12] / np,
+              1e3 * d[11] / std::max(1.0, (double)d[9]), 1e3 * d[12] / std::max(1.0, (double)d[10]));
     }
     h->launches += 2;   // flag memset + kernel
     return FRAM_OK;

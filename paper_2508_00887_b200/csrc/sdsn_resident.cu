@@ -48,10 +48,10 @@ template <int CPT> struct RC {
 constexpr int kResMaxRows = 32;             // rows per CTA (the grid is sized so R ≤ 32)
 constexpr int kResKMax = 5;                  // G ≤ 32·kResKMax CTAs (148 SMs)
 
-// dynamic shared memory: SMEM-resident rows, column staging, per-thread row partials, s_r, s_a
+// dynamic shared memory: SMEM-resident rows, column staging, per-warp row partials, s_r, s_rn
 size_t res_smem_bytes(int cpt, int rs, int R) {
   const size_t ns = 128 * (size_t)cpt;
-  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 8 * 4 + (size_t)R * 8 + (size_t)R * 4 + 64;
+  return (size_t)rs * ns * 4 + ns * 4 + (size_t)R * 8 * 4 + (size_t)R * 8 + (size_t)R * 8 + 64;
 }
 
 template <int CPT> struct RK {
@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   float4* s_col = s_rows + (size_t)RS * V * 128;                      // [V·128] column staging
   float* s_rowpart = reinterpret_cast<float*>(s_col + V * 128);       // [Rmax][8] per-warp row partials
   double* s_r = reinterpret_cast<double*>(s_rowpart + Rmax * 8);     // [Rmax] row sums (FP64)
-  float* s_a = reinterpret_cast<float*>(s_r + Rmax);                 // [Rmax] a_i (FP32)
+  double* s_rn = s_r + Rmax;                                          // [Rmax] r_i / n (FP64)
   __shared__ uint32_t s_tmem;
   __shared__ double s_red[NW];
   __shared__ double s_S;
@@ -182,9 +182,10 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   if (P.scale) {
     if (warp == 0) {
       double mm = 0.0;
+      double v[kResKMax];
+      wait_d1_lanes<kResKMax>(P.Mpart, G, lane, 1u, v);
 #pragma unroll
-      for (int i = 0; i < kResKMax; ++i)
-        if (lane + 32 * i < G) mm = fmax(mm, wait_d1(P.Mpart + lane + 32 * i, 1u));
+      for (int i = 0; i < kResKMax; ++i) mm = fmax(mm, v[i]);
       mm = warp_max_d(mm);
       if (lane == 0) s_S = mm;
     }
@@ -209,7 +210,20 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
 
   // after a sweep: column partials (two row groups combined in shared memory) → colpart[b];
   // row sums (per-lane partials → fixed-order tree) → s_r; Σ r → Spart[b]; all tagged e
-  long long tfine[4] = {0, 0, 0, 0};
+  // dev timing (P.dbg, FRAM_RES_TIMING): per-CTA slots accumulated in shared memory by one thread
+  // (k < 9) or by the first warp of each row group (rows: 9 + g ns, 11 + g cycles), copied out at the end
+  __shared__ long long s_dbg[16];
+  if (tid < 16) s_dbg[tid] = 0;
+  __syncthreads();
+  auto dadd = [&](int k, long long v) { if (P.dbg && tid == 0) s_dbg[k] += v; };
+  int jst = -1;                                          // pass whose timeline is stamped (dev timing)
+  auto stamp = [&](int k) {
+    if (P.dbg && tid == 0 && jst == 500) {
+      long long v;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+      P.dbg[(size_t)G * 16 + b * 8 + k] = v;
+    }
+  };
   auto gt = [&]() -> long long {
     long long v = 0;
     if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
@@ -234,26 +248,23 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
         st_w4(dst + (size_t)((c0 + c) * 128 + t) * 4, make_uint4(ptag(o.x, e), ptag(o.y, e), ptag(o.z, e), ptag(o.w, e)));
       }
     }
-    const long long e1a = gt();
-    // row sums: the 4·NH per-warp partials of each row, combined in FP64 in a fixed order
-    for (int i = tid; i < R; i += THREADS) {
-      const float* pp = s_rowpart + i * 8;
+    // row sums, off the critical path (group 0 goes on to the slice reduction): the first warp of
+    // group 1 combines the 4·NH per-warp partials of row `lane` in FP64 in a fixed order, keeps
+    // r_i and r_i/n, and publishes this CTA's Σ r_i (R ≤ 32 rows: one row per lane)
+    if (warp == NW / 2) {
       double acc = 0.0;
+      if (lane < R) {
+        const float* pp = s_rowpart + lane * 8;
 #pragma unroll
-      for (int k = 0; k < 4 * K::NH; ++k) acc += (double)pp[k];
-      s_r[i] = acc;
+        for (int k = 0; k < 4 * K::NH; ++k) acc += (double)pp[k];
+        s_r[lane] = acc;
+        s_rn[lane] = acc / dn;
+      }
+      const double sp = warp_sum_d(acc);
+      if (lane == 0 && e != 0) st_d1(P.Spart + (size_t)(e & 1) * G + b, sp, (e >> 1) & 1u);
     }
-    const long long e1b = gt();
-    __syncthreads();
-    const long long e1c = gt();
-    if (warp == 0 && e != 0) {
-      double s = 0.0;
-      for (int i = lane; i < R; i += 32) s += s_r[i];
-      s = warp_sum_d(s);
-      if (lane == 0) st_d1(P.Spart + (size_t)(e & 1) * G + b, s, (e >> 1) & 1u);
-    }
-    const long long e2 = gt();
-    tfine[1] += e1a - e1; tfine[2] += e1b - e1a; tfine[3] += e1c - e1b; tfine[0] += e2 - e1c;
+    const long long e1a = gt();
+    dadd(4, e1a - e1);
   };
   // this warp's partials of rows ra and rb (rb < 0: none): two interleaved shuffle trees, lane 0
   // stores them at slot 4·h + q of the row (fixed order, deterministic)
@@ -267,6 +278,25 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
     if (lane == 0) s_rowpart[ra * 8 + 4 * h + q] = keep;
     if (lane == 16 && rb >= 0) s_rowpart[rb * 8 + 4 * h + q] = keep;
+  };
+  // this warp's partials of the NB rows i0 + k·rstep (k < NB, rows ≥ rend absent): one transpose-
+  // reduce — each xor level (16, 8, …) halves the set of rows a lane carries, the remaining levels
+  // finish the sum (NB = 8: 9 shuffles for 8 rows); lane k·32/NB ends with row k.  Fixed tree.
+  auto put_rowparts_n = [&](auto nb, int i0, int rstep, int rend, float* v) {
+    constexpr int NB = decltype(nb)::value;
+    constexpr int LG = NB == 8 ? 3 : NB == 4 ? 2 : 1;
+#pragma unroll
+    for (int l = 0; l < LG; ++l) {
+      const int off = 16 >> l, m = NB >> (l + 1);
+      const bool hi = lane & off;
+#pragma unroll
+      for (int i = 0; i < m; ++i) v[i] = (hi ? v[i + m] : v[i]) + __shfl_xor_sync(0xffffffffu, hi ? v[i] : v[i + m], off);
+    }
+    float z = v[0];
+#pragma unroll
+    for (int off = 16 >> LG; off > 0; off >>= 1) z += __shfl_xor_sync(0xffffffffu, z, off);
+    const int r = i0 + (lane >> (5 - LG)) * rstep;
+    if ((lane & ((32 >> LG) - 1)) == 0 && r < rend) s_rowpart[r * 8 + 4 * h + q] = z;
   };
 
   // Y0 = fl(s·X) (Alg.2 step 1; skipped when !P.scale) with its sums
@@ -308,49 +338,100 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     }
     return rs.x + rs.y;
   };
+  double abase = 0.0;                                    // 1/n + S/n² of the current pass
+  auto arow = [&](int r) -> float { return (float)(abase - s_rn[r]); };   // a_i (FP64, rounded once)
   auto sweep_pass = [&](const float2 (&bv)[CH / 2], unsigned e) {
     const long long l0 = gt();
+    const long long c0k = P.dbg ? clock64() : 0;
     float2 col2[CH / 2];
 #pragma unroll
     for (int k = 0; k < CH / 2; ++k) col2[k] = make_float2(0.f, 0.f);
     // rows of this row group: with rows in both TMEM and shared memory, group 0 takes the TMEM rows
     // and group 1 the shared-memory rows so the two datapaths work concurrently; otherwise rows
-    // alternate between the groups
-    int rbeg, rend, rstep;
-    if (R > RT) { rbeg = g == 0 ? 0 : RT; rend = g == 0 ? RT : R; rstep = 1; }
-    else { rbeg = g; rend = R; rstep = 2; }
-    int ra = rbeg;
-    for (; ra + rstep < rend; ra += 2 * rstep) {         // two rows at a time
-      const int rb = ra + rstep;
-      float xa[CH], xb[CH];
-      if (rb < RT) {                                     // both rows in TMEM: one wait for two loads
-        uint32_t va[CH], vb[CH];
-        tmem_ld<CH>(tmem + (uint32_t)(ra * CPT), va);
-        tmem_ld<CH>(tmem + (uint32_t)(rb * CPT), vb);
-        tmem_wait_ld();
+    // alternate between the groups.  Each datapath has its own loop (no per-row kind test).
+    // A warp's rows rbeg, rbeg + rstep, … < rend go in batches of 8 (4 pairs); the per-lane row
+    // partials of a batch stay in registers and are reduced together by put_rowparts8 after the
+    // batch, so no shuffle chain sits between one pair's stores and the next pair's loads.
+    auto rows_tmem = [&](int rbeg, int rend, int rstep) {
+      for (int i0 = rbeg; i0 < rend; i0 += 8 * rstep) {
+        float rsv[8];
 #pragma unroll
-        for (int k = 0; k < CH; ++k) { xa[k] = __uint_as_float(va[k]); xb[k] = __uint_as_float(vb[k]); }
-      } else {
-        load_row(ra, xa);
-        load_row(rb, xb);
+        for (int i = 0; i < 8; i += 2) {
+          const int ra = i0 + i * rstep, rb = ra + rstep;
+          rsv[i] = 0.f;
+          rsv[i + 1] = 0.f;
+          if (rb < rend) {                               // two rows, one wait for both loads
+            uint32_t va[CH], vb[CH];
+            tmem_ld<CH>(tmem + (uint32_t)(ra * CPT), va);
+            tmem_ld<CH>(tmem + (uint32_t)(rb * CPT), vb);
+            tmem_wait_ld();
+            float xa[CH], xb[CH];
+#pragma unroll
+            for (int k = 0; k < CH; ++k) { xa[k] = __uint_as_float(va[k]); xb[k] = __uint_as_float(vb[k]); }
+            rsv[i] = pass_rows(xa, arow(ra), bv, col2);
+            rsv[i + 1] = pass_rows(xb, arow(rb), bv, col2);
+#pragma unroll
+            for (int k = 0; k < CH; ++k) { va[k] = __float_as_uint(xa[k]); vb[k] = __float_as_uint(xb[k]); }
+            tmem_st<CH>(tmem + (uint32_t)(ra * CPT), va);
+            tmem_st<CH>(tmem + (uint32_t)(rb * CPT), vb);
+          } else if (ra < rend) {
+            float xa[CH];
+            load_row(ra, xa);
+            rsv[i] = pass_rows(xa, arow(ra), bv, col2);
+            store_row(ra, xa);
+          }
+        }
+        put_rowparts_n(std::integral_constant<int, 8>{}, i0, rstep, rend, rsv);
       }
-      const float sa = pass_rows(xa, s_a[ra], bv, col2);
-      const float sb = pass_rows(xb, s_a[rb], bv, col2);
-      store_row(ra, xa);
-      store_row(rb, xb);
-      put_rowparts(ra, sa, rb, sb);
-    }
-    if (ra < rend) {
-      float xa[CH];
-      load_row(ra, xa);
-      const float sa = pass_rows(xa, s_a[ra], bv, col2);
-      store_row(ra, xa);
-      put_rowparts(ra, sa, -1, 0.f);
+    };
+    auto rows_smem = [&](int rbeg, int rend) {
+      for (int i0 = rbeg; i0 < rend; i0 += 4) {
+        float rsv[4];
+#pragma unroll
+        for (int i = 0; i < 4; i += 2) {
+          const int ra = i0 + i;
+          rsv[i] = 0.f;
+          rsv[i + 1] = 0.f;
+          if (ra + 1 < rend) {
+            float4* pa = s_rows + (size_t)(ra - RT) * (V * 128) + c0 * 128 + t;
+            float4* pb = pa + V * 128;
+            float xa[CH], xb[CH];
+#pragma unroll
+            for (int c = 0; c < VH; ++c) {
+              const float4 u = pa[c * 128], w = pb[c * 128];
+              xa[4 * c] = u.x; xa[4 * c + 1] = u.y; xa[4 * c + 2] = u.z; xa[4 * c + 3] = u.w;
+              xb[4 * c] = w.x; xb[4 * c + 1] = w.y; xb[4 * c + 2] = w.z; xb[4 * c + 3] = w.w;
+            }
+            rsv[i] = pass_rows(xa, arow(ra), bv, col2);
+            rsv[i + 1] = pass_rows(xb, arow(ra + 1), bv, col2);
+#pragma unroll
+            for (int c = 0; c < VH; ++c) {
+              pa[c * 128] = make_float4(xa[4 * c], xa[4 * c + 1], xa[4 * c + 2], xa[4 * c + 3]);
+              pb[c * 128] = make_float4(xb[4 * c], xb[4 * c + 1], xb[4 * c + 2], xb[4 * c + 3]);
+            }
+          } else if (ra < rend) {
+            float xa[CH];
+            load_row(ra, xa);
+            rsv[i] = pass_rows(xa, arow(ra), bv, col2);
+            store_row(ra, xa);
+          }
+        }
+        put_rowparts_n(std::integral_constant<int, 4>{}, i0, 1, rend, rsv);
+      }
+    };
+    if (R > RT) {
+      if (g == 0) rows_tmem(0, RT, 1);
+      else rows_smem(RT, R);
+    } else {
+      rows_tmem(g, R, 2);
     }
     float col[CH];
 #pragma unroll
     for (int k = 0; k < CH / 2; ++k) { col[2 * k] = col2[k].x; col[2 * k + 1] = col2[k].y; }
-    (void)l0;
+    if (P.dbg && lane == 0 && (warp & 7) == 0) {
+      s_dbg[9 + g] += gt() - l0;
+      s_dbg[11 + g] += clock64() - c0k;
+    }
     sweep_epilogue(col, e);
   };
 
@@ -383,6 +464,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       }
       s_red2[warp][lane] = acc;
       __syncthreads();
+      if (sb == s0) stamp(4);
       if (warp == 0 && s < s1) {
         double cs = 0.0;
 #pragma unroll
@@ -397,9 +479,10 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   // S of epoch e (row-sum partials, parity buffer), waited for by one warp while the others wait for b
   auto wait_S = [&](unsigned e) {
     double sacc = 0.0;
+    double v[kResKMax];
+    wait_d1_lanes<kResKMax>(P.Spart + (size_t)(e & 1) * G, G, lane, (e >> 1) & 1u, v);
 #pragma unroll
-    for (int i = 0; i < kResKMax; ++i)
-      if (lane + 32 * i < G) sacc += wait_d1(P.Spart + (size_t)(e & 1) * G + lane + 32 * i, (e >> 1) & 1u);
+    for (int i = 0; i < kResKMax; ++i) sacc += v[i];      // absent words are +0: same sum as before
     sacc = warp_sum_d(sacc);
     if (lane == 0) s_S = sacc;
   };
@@ -415,21 +498,24 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   // ---------------- pass loop (device-side stop decision, identical in every CTA) ----------------
   int j = 0;
   double gam = 0.0;
-  long long tacc[6] = {0, 0, 0, 0, 0, 0};   // dev timing (P.dbg): bload, sweep, -, slice, -
   auto now = [&]() -> long long {
     long long v = 0;
     if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
     return v;
   };
   for (;; ++j) {
+    jst = j;
+    stamp(0);
     long long t0 = now();
-    // pass boundary: every thread waits for its b values of epoch ep while warp 1 also collects S
+    // pass boundary: row group 0 waits for the b values of epoch ep (its columns are those of group
+    // 1) and hands them to group 1 through shared memory (s_col), while the first warp of group 1
+    // collects S — half the L2 polling traffic of every thread polling its own words
     float2 bv[CH / 2];                                   // b_j pairs (register pairs for FADD2)
-    {
+    if (g == 0) {
       uint4 w[VH];
+      const unsigned* myb = P.bvec;
 #pragma unroll
-      for (int c = 0; c < VH; ++c) w[c] = ld_w4(P.bvec + (size_t)((c0 + c) * 128 + t) * 4);
-      if (warp == 1) wait_S(ep);
+      for (int c = 0; c < VH; ++c) w[c] = ld_w4(myb + (size_t)((c0 + c) * 128 + t) * 4);
       bool ok;
       do {                                               // wait for every b of epoch ep
         ok = true;
@@ -437,44 +523,57 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
         for (int c = 0; c < VH; ++c) {
           if (!pok(w[c].x, ep) || !pok(w[c].y, ep) || !pok(w[c].z, ep) || !pok(w[c].w, ep)) {
             ok = false;
-            w[c] = ld_w4(P.bvec + (size_t)((c0 + c) * 128 + t) * 4);
+            w[c] = ld_w4(myb + (size_t)((c0 + c) * 128 + t) * 4);
           }
         }
       } while (!ok);
+      stamp(1);
 #pragma unroll
       for (int c = 0; c < VH; ++c) {                     // b = −|b|; −0 and −∞ (padding) as stored
-        bv[2 * c] = make_float2(-pval(w[c].x), -pval(w[c].y));
-        bv[2 * c + 1] = make_float2(-pval(w[c].z), -pval(w[c].w));
+        const float4 v = make_float4(-pval(w[c].x), -pval(w[c].y), -pval(w[c].z), -pval(w[c].w));
+        s_col[(c0 + c) * 128 + t] = v;
+        bv[2 * c] = make_float2(v.x, v.y);
+        bv[2 * c + 1] = make_float2(v.z, v.w);
       }
+    } else if (warp == NW / 2) {
+      wait_S(ep);
     }
     __syncthreads();
-    const double S = s_S;                               // written by warp 1 (wait_S), synced
+    if (g == 1) {
+#pragma unroll
+      for (int c = 0; c < VH; ++c) {
+        const float4 v = s_col[(c0 + c) * 128 + t];
+        bv[2 * c] = make_float2(v.x, v.y);
+        bv[2 * c + 1] = make_float2(v.z, v.w);
+      }
+    }
+    stamp(2);
+    const double S = s_S;                               // written by wait_S, synced
     gam = S / dn - 1.0;                                                 // γ_j
     if (b == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[j] = gam;
     const bool last = P.sdsn_fixed > 0 ? (j + 1 >= P.sdsn_fixed)
                                        : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
-    const double abase = 1.0 / dn + S / nn;
-    for (int i = tid; i < R; i += THREADS) s_a[i] = (float)(abase - s_r[i] / dn);
-    __syncthreads();
+    abase = 1.0 / dn + S / nn;
     long long t1 = now();
     sweep_pass(bv, last ? 0u : ep + 1);
-    __syncthreads();
     long long t2 = now();
-    if (last) break;
+    stamp(3);
+    if (last) {
+      __syncthreads();
+      break;
+    }
     ++ep;
-    slice(ep);
-    __syncthreads();
+    slice(ep);                                           // ends with a block barrier
+    stamp(5);
     long long t4 = now();
-    tacc[0] += t1 - t0; tacc[1] += t2 - t1; tacc[3] += t4 - t2;
-    tacc[5] += 1;
+    dadd(0, t1 - t0); dadd(1, t2 - t1); dadd(8, t4 - t2);
   }
   if (P.dbg && tid == 0) {
-    for (int k = 0; k < 6; ++k) P.dbg[b * 8 + k] = tacc[k];
-    P.dbg[b * 8 + 2] = tfine[0]; P.dbg[b * 8 + 4] = tfine[1]; P.dbg[b * 8 + 6] = tfine[2]; P.dbg[b * 8 + 7] = tfine[3];
+    for (int k = 0; k < 16; ++k) P.dbg[b * 16 + k] = s_dbg[k];
     long long tk2;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk2));
-    P.dbg[b * 8 + 5] = (tacc[5] & 0xffff) | ((tk1 - tk0) << 16);   // passes | load-phase ns
-    P.dbg[b * 8 + 3] = tk2 - tk0;                                   // total ns to loop end
+    P.dbg[b * 16 + 5] = (j & 0xffff) | ((tk1 - tk0) << 16);         // passes | load-phase ns
+    P.dbg[b * 16 + 3] = tk2 - tk0;                                   // total ns to loop end
   }
 
   // ---------------- D = Y_final → global (row-major, ld) ----------------

@@ -48,6 +48,24 @@ __device__ __forceinline__ double wait_d1(const uint64_t* p, unsigned bit) {
   return __longlong_as_double((long long)(w & 0x7fffffffffffffffull));
 }
 
+// NW tagged FP64 words p[lane + 32·i] (i < NW, index < cnt; absent words read as 0): all loads are
+// issued before any is waited on, so the wait costs one L2 round trip, not NW of them
+template <int NW>
+__device__ __forceinline__ void wait_d1_lanes(const uint64_t* p, int cnt, int lane, unsigned bit, double (&out)[NW]) {
+  uint64_t w[NW];
+#pragma unroll
+  for (int i = 0; i < NW; ++i) w[i] = lane + 32 * i < cnt ? ld_tag(p + lane + 32 * i) : ((uint64_t)bit << 63);
+  bool ok;
+  do {
+    ok = true;
+#pragma unroll
+    for (int i = 0; i < NW; ++i)
+      if ((unsigned)(w[i] >> 63) != bit) { ok = false; w[i] = ld_tag(p + lane + 32 * i); }
+  } while (!ok);
+#pragma unroll
+  for (int i = 0; i < NW; ++i) out[i] = __longlong_as_double((long long)(w[i] & 0x7fffffffffffffffull));
+}
+
 // two FP32 adds in one instruction (FADD2, sm_100): d = (a.x + b.x, a.y + b.y), each RN
 __device__ __forceinline__ float2 add2(float2 a, float2 b) {
   float2 d;
