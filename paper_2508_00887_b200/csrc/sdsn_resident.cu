@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   using C = RC<CPT>;
   using K = RK<CPT>;
   constexpr int V = C::V, NS = C::NS, RT = C::RT;
-  constexpr int NW = K::NW, CH = K::CH, VH = K::VH, THREADS = K::THREADS;
+  constexpr int NW = K::NW, CH = K::CH, VH = K::VH;
   extern __shared__ __align__(16) unsigned char dsm[];
   const int RS = P.rs;
   const int Rmax = P.rmax;
@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   auto sweep_epilogue = [&](const float (&col)[CH], unsigned e) {
     const long long e0 = gt();
     tmem_wait_st();
+    // the two row groups' column partials are combined through shared memory and published by
+    // group 0 (splitting the stores between the groups measured slower)
     if (g == 1) {
 #pragma unroll
       for (int c = 0; c < VH; ++c)
@@ -466,14 +468,19 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       __syncthreads();
       if (sb == s0) stamp(4);
       if (warp == 0 && s < s1) {
-        double cs = 0.0;
+        double v[NW];                                    // the NW warp sums, fixed pairwise tree
 #pragma unroll
-        for (int w = 0; w < NW; ++w) cs += s_red2[w][lane];
+        for (int w = 0; w < NW; ++w) v[w] = s_red2[w][lane];
+#pragma unroll
+        for (int st = 1; st < NW; st *= 2)
+#pragma unroll
+          for (int w = 0; w < NW; w += 2 * st) v[w] += v[w + st];
+        const double cs = v[0];
         const int f = s >> 2, e4 = s & 3, c = f >> 7, tt = f & 127;
         const long colj = (long)tt * CPT + 4 * c + e4;
         st_w(P.bvec + s, ptag(colj < n ? (float)(cs / dn) : CUDART_INF_F, e));   // |b_j| = c_j/n
       }
-      __syncthreads();
+      if (sb + 32 < s1) __syncthreads();               // s_red2 is reused by the next chunk
     }
   };
   // S of epoch e (row-sum partials, parity buffer), waited for by one warp while the others wait for b
@@ -563,7 +570,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       break;
     }
     ++ep;
-    slice(ep);                                           // ends with a block barrier
+    slice(ep);
     stamp(5);
     long long t4 = now();
     dadd(0, t1 - t0); dadd(1, t2 - t1); dadd(8, t4 - t2);
