@@ -136,15 +136,24 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
       const int i0n = p[j1];                          // p is not modified during a search
       if (i0n != 0) load_row(i0n);                    // next row's loads overlap the updates below
       // potentials: used columns (u[p[j]] += δ, v[j] −= δ), virtual column 0 (u[i] += δ), free minv −= δ
+      // The used columns' rows prow[k] are distinct (one owner per column), so all u loads are issued
+      // before any store: the read-modify-writes overlap instead of forming one latency chain.
       const Mask usd = inr & ~fr;
+      double ut[CPT];
+#pragma unroll
+      for (int k = 0; k < CPT; ++k)
+        if ((usd >> k) & one) ut[k] = u[prow[k]];
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
         if ((usd >> k) & one) {
-          u[prow[k]] = __dadd_rn(u[prow[k]], delta);
+          ut[k] = __dadd_rn(ut[k], delta);
           v[k] = __dsub_rn(v[k], delta);
         }
         minv[k] = __dsub_rn(minv[k], delta);         // free: as the oracle; used/absent: +inf stays +inf
       }
+#pragma unroll
+      for (int k = 0; k < CPT; ++k)
+        if ((usd >> k) & one) u[prow[k]] = ut[k];
       if (tid == 0) u[i] = __dadd_rn(u[i], delta);
       j0 = j1;
       i0 = i0n;

@@ -55,14 +55,43 @@ __global__ void __launch_bounds__(512, 1) sweep(int passes, float* out, long lon
   for (int k = 0; k < CH / 2; ++k) bv[k] = make_float2(-0.0001f * k, -0.0002f);
   __syncthreads();
 
+  auto relu = [&](float v) -> float {
+    if (MODE == 3) return __int_as_float(max(__float_as_int(v), 0));
+    if (MODE == 4) return v;
+    return fmaxf(0.0f, v);
+  };
   auto pass_row = [&](float (&x)[CH], float a, float2 (&col2)[CH / 2]) -> float {
     float2 rs = make_float2(0.f, 0.f);
     const float2 a2 = make_float2(a, a);
+    if (MODE == 5) {                    // scalar FADDs
+      float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+      for (int k = 0; k < CH; k += 2) {
+        float y0 = fmaxf(0.f, (x[k] + a) + bv[k / 2].x), y1 = fmaxf(0.f, (x[k + 1] + a) + bv[k / 2].y);
+        x[k] = y0; x[k + 1] = y1;
+        col2[k / 2].x += y0; col2[k / 2].y += y1;
+        r0 += y0; r1 += y1;
+      }
+      return r0 + r1;
+    }
+    if (MODE == 6) {                    // FADD2 with two independent row-sum chains
+      float2 r0 = make_float2(0.f, 0.f), r1 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < CH; k += 2) {
+        float2 y = add2(add2(make_float2(x[k], x[k + 1]), a2), bv[k / 2]);
+        y.x = fmaxf(0.0f, y.x); y.y = fmaxf(0.0f, y.y);
+        x[k] = y.x; x[k + 1] = y.y;
+        col2[k / 2] = add2(col2[k / 2], y);
+        if (k & 2) r1 = add2(r1, y); else r0 = add2(r0, y);
+      }
+      r0 = add2(r0, r1);
+      return r0.x + r0.y;
+    }
 #pragma unroll
     for (int k = 0; k < CH; k += 2) {
       float2 y = add2(add2(make_float2(x[k], x[k + 1]), a2), bv[k / 2]);
-      y.x = fmaxf(0.0f, y.x);
-      y.y = fmaxf(0.0f, y.y);
+      y.x = relu(y.x);
+      y.y = relu(y.y);
       x[k] = y.x;
       x[k + 1] = y.y;
       col2[k / 2] = add2(col2[k / 2], y);
@@ -126,7 +155,44 @@ __global__ void __launch_bounds__(512, 1) sweep(int passes, float* out, long lon
         put2(50 + r, sa, r + 1 < G1 ? 51 + r : -1, sb);
       }
     }
-    if (MODE == 1) {
+    if (MODE == 7) {                      // compute only, four rows interleaved
+      const int nrows = tcnt + scnt;
+      for (int rb8 = 0; rb8 < nrows; rb8 += 8) {
+        float rsv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 4) {
+          float2 r[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) r[u] = make_float2(0.f, 0.f);
+          const float2 a2 = make_float2(a, a);
+#pragma unroll
+          for (int k = 0; k < CH; k += 2) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              float2 y = add2(add2(make_float2(reg[u][k], reg[u][k + 1]), a2), bv[k / 2]);
+              y.x = fmaxf(0.f, y.x); y.y = fmaxf(0.f, y.y);
+              reg[u][k] = y.x; reg[u][k + 1] = y.y;
+              col2[k / 2] = add2(col2[k / 2], y);
+              r[u] = add2(r[u], y);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rsv[i + u] = r[u].x + r[u].y;
+        }
+        put8(rb8, rsv, nrows - rb8);
+      }
+    } else if (MODE >= 2) {                      // compute only: the same two register rows, no loads/stores
+      const int nrows = tcnt + scnt;
+      for (int rb8 = 0; rb8 < nrows; rb8 += 8) {
+        float rsv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+          rsv[i] = 0.f; rsv[i + 1] = 0.f;
+          if (rb8 + i + 1 < nrows) { rsv[i] = pass_row(reg[0], a, col2); rsv[i + 1] = pass_row(reg[1], a, col2); }
+        }
+        put8(rb8, rsv, nrows - rb8);
+      }
+    } else if (MODE == 1) {
       for (int rb8 = tbeg; rb8 < tbeg + tcnt; rb8 += 8) {
         float rsv[8];
 #pragma unroll
@@ -268,13 +334,7 @@ void run(const char* name) {
 }
 
 int main() {
-  run<16, 0, 0, 0, 12, 0, 0>("K4r layout, pair reduce");
-  run<16, 0, 0, 0, 12, 0, 1>("K4r layout, 8-row deferred reduce");
-  run<16, 0, 0, 0, 0, 0, 0>("TMEM only, pair reduce");
-  run<16, 0, 0, 0, 0, 0, 1>("TMEM only, deferred");
-  run<0, 0, 0, 0, 12, 0, 0>("SMEM only, pair reduce");
-  run<0, 0, 0, 0, 12, 0, 1>("SMEM only, deferred");
-  run<8, 6, 0, 8, 6, 0, 1>("both kinds both groups, deferred");
-  run<16, 0, 0, 0, 12, 0, 1>("K4r layout, deferred (again)");
+  run<16, 0, 4, 0, 12, 4, 2>("compute only, FADD2 pairs");
+  run<16, 0, 4, 0, 12, 4, 7>("compute only, FADD2 quads");
   return 0;
 }
