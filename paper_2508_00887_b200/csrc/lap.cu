@@ -61,6 +61,7 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
 
   // column j = 1 + tid + k·THREADS lives in this thread's registers
   double minv[CPT], v[CPT], cv[CPT];
+  double vs[CPT];                                     // scan copy of v: −inf for used / absent columns
   int prow[CPT];                                      // row owning a USED column (fixed during a search)
   using Mask = typename std::conditional<(CPT > 32), uint64_t, uint32_t>::type;
   constexpr Mask one = 1;
@@ -84,14 +85,19 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
   for (int i = 1; i <= n; ++i) {
     Mask fr = inr;                                    // bit k: column free (not yet in the tree)
 #pragma unroll
-    for (int k = 0; k < CPT; ++k) minv[k] = CUDART_INF;
+    for (int k = 0; k < CPT; ++k) {
+      minv[k] = CUDART_INF;
+      vs[k] = ((inr >> k) & one) ? v[k] : -CUDART_INF;
+    }
     if (tid == 0) p[0] = i;                           // read only by thread 0's augmentation
     int j0 = 0, i0 = i;
     load_row(i0);
     while (true) {
       // used[j0] = true (the owner remembers p[j0] = i0 for the potential updates).  A used column's
       // minv is never read again in this search (oracle: only free columns are scanned and updated),
-      // so it is parked at +inf: the scan and the `minv −= δ` update then need no free-column mask.
+      // so it is parked at +inf, and its scan copy of v at −inf (its cur is then +inf, never < minv):
+      // the scan and the `minv −= δ` update need no free-column mask.  A free column's v does not
+      // change during a search, so vs = v there and cur is the oracle's value.
       if (j0 > 0 && ((j0 - 1) % THREADS) == tid) {
         const int kk = (j0 - 1) / THREADS;
         fr &= ~(one << kk);
@@ -99,15 +105,15 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
         for (int k = 0; k < CPT; ++k) {
           prow[k] = (k == kk) ? i0 : prow[k];
           minv[k] = (k == kk) ? CUDART_INF : minv[k];
+          vs[k] = (k == kk) ? -CUDART_INF : vs[k];
         }
       }
       const double ui0 = u[i0];                       // not written during this step (i0 ∉ tree)
       double bv[CPT];
 #pragma unroll
       for (int k = 0; k < CPT; ++k) {
-        const bool f = (fr >> k) & one;
-        const double cur = __dsub_rn(__dsub_rn(-cv[k], ui0), v[k]);     // (C[i0][j] − u[i0]) − v[j]
-        const bool upd = f && cur < minv[k];
+        const double cur = __dsub_rn(__dsub_rn(-cv[k], ui0), vs[k]);    // (C[i0][j] − u[i0]) − v[j]
+        const bool upd = cur < minv[k];
         minv[k] = upd ? cur : minv[k];
         if (upd) way[1 + tid + k * THREADS] = j0;
         bv[k] = minv[k];                              // +inf for used / absent columns
