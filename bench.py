@@ -309,15 +309,19 @@ def run_ours(args):
     if resident:
         # K4r keeps Y on chip (TMEM + shared memory): HBM is touched only to load G and store D once per
         # launch, so the pass loop is bound by the SM datapath.  Roofline: 5 FP32 ops per
-        # element per pass (x+a, +b, max, column and row accumulation) against the issue-bound ALU
-        # peak for that op mix: 148 SMs x 128 lanes x f_max, x 5/3 (the 4 adds issue as 2 paired FADD2).
+        # element per pass (x+a, +b, max, column and row accumulation).  The four adds run on the FP32
+        # lanes (128 per SM per cycle; a paired FADD2 issues in 2 cycles, measured by tools/pipe_probe.cu)
+        # while the max overlaps on the ALU pipe, so the element rate is 148 x 128 x f_max / 4 and the
+        # op peak is 5/4 of the FP32 lane rate: 46.5 TFLOP/s at 1.965 GHz.
         f_max = 1.965e9
-        alu_peak = 148 * 128 * f_max * 5.0 / 3.0 / 1e12
+        alu_peak = 148 * 128 * f_max * 5.0 / 4.0 / 1e12
         achieved = 5.0 * n * n * passes_per_launch / avg_launch_s / 1e12
         roof = {"kernel": "sdsn_res_kernel<32> (K4r, on-chip resident; one persistent launch per SDSN call)",
                 "bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "TFLOP/s",
                 "frac": achieved / alu_peak, "traffic": traffic,
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 1.965 GHz x 5/3 (B200_PROFILING.md unit counts)",
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 1.965 GHz x 5/4 (4 FP32 adds per element on the "
+                               "FP32 lanes, the max overlapped on the ALU pipe; B200_PROFILING.md unit counts, "
+                               "FADD2 rate measured by tools/pipe_probe.cu)",
                 "algorithmic_flops_per_launch": 5.0 * n * n * passes_per_launch,
                 "hbm_equivalent": {"achieved_gbs": hbm_equiv, "peak_gbs": hbm, "frac": hbm_equiv / hbm,
                                    "note": "algorithmic 8n^2 B/pass over the launch time; the iterate never leaves the chip"}}
