@@ -92,6 +92,14 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   const long r0 = (long)b * n / G, r1 = (long)(b + 1) * n / G;
   const int R = (int)(r1 - r0);
   const double dn = (double)n, nn = dn * dn;
+  // S/n and S/n² on the pass-start critical path without a full FP64 division: with the correctly
+  // rounded reciprocal r = RN(1/d), q = RN(S·r) and one FMA correction q + r·(S − q·d) is RN(S/d)
+  // (Markstein's theorem; tools/div_probe.cu: 0 mismatches against IEEE division in 3.6e10 cases)
+  const double rn = __drcp_rn(dn), rnn = __drcp_rn(nn);
+  auto div_n = [&](double S_, double d, double r) {
+    const double q = S_ * r;
+    return fma(r, fma(-q, d, S_), q);
+  };
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -556,11 +564,11 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     }
     stamp(2);
     const double S = s_S;                               // written by wait_S, synced
-    gam = S / dn - 1.0;                                                 // γ_j
+    gam = div_n(S, dn, rn) - 1.0;                                       // γ_j = S/n − 1
     if (b == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[j] = gam;
     const bool last = P.sdsn_fixed > 0 ? (j + 1 >= P.sdsn_fixed)
                                        : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
-    abase = 1.0 / dn + S / nn;
+    abase = rn + div_n(S, nn, rnn);                                     // 1/n + S/n²
     long long t1 = now();
     sweep_pass(bv, last ? 0u : ep + 1);
     long long t2 = now();
