@@ -158,7 +158,7 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
   CK(h->UT.ensure(nn * op_size(op)), "alloc U");
   CK(h->Y.ensure(nn * (f64 ? 8 : 4)), "alloc G/Y");
   CK(h->colpart.ensure((size_t)G * ld * (f64 ? 8 : 4)), "alloc colpart");
-  CK(h->Spart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Spart");
+  CK(h->Spart.ensure(2 * (size_t)std::max(G, h->num_sms) * 8), "alloc Spart");   // [2][G] tagged (K4)
   CK(h->Mpart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Mpart");
   if (!f64 && fram::sdsn_res_grid(n, h->num_sms) > 0) {
     CK(h->rcolpart.ensure(fram::sdsn_res_xchg_words(n, h->num_sms) * 8), "alloc resident exchange");

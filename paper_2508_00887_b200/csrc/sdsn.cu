@@ -14,16 +14,51 @@
 // ring keeping PD rows of 16-byte loads in flight (no CTA barrier inside the sweep):
 //   row sums : warp shuffle per row → s_rowpart[row][cg] → fixed-order sum over cg (FP64);
 //   col sums : per-lane register partials over the warp's rows → (RG>1: fixed-order smem combine)
-//              → colpart[b][:] → grid barrier → CTA b reduces column slice b over all CTAs in a
-//              fixed order (deterministic, no float atomics: S:375) → grid barrier;
+//              → colpart[b][:] → CTA b reduces column slice b over all CTAs in a fixed order
+//              (deterministic, no float atomics: S:375) → c (FP64) → read by every CTA;
 //   S        : Σ per-CTA row-sum partials, summed identically by every CTA (FP64).
+// No grid barriers: every exchanged word carries its epoch's parity in the sign bit (the values
+// are non-negative) and is re-read until the tag matches (the K4r exchange, xchg.cuh).
 // Algorithmic bytes per pass: 8n² (FP32) / 16n² (FP64) of Y, + O(G·n) of partials.
 #include <stdlib.h>
 #include <type_traits>
 #include "common.cuh"
 #include "internal.h"
+#include "xchg.cuh"
 
 namespace fram {
+
+// Tagged words of the cross-CTA exchange (as in K4r, xchg.cuh): non-negative values with the epoch
+// parity in the sign bit; a consumer re-reads a word until its tag matches, so no grid barrier is
+// needed.  T = float: 4-byte words; T = double: 8-byte words.
+template <typename T> struct Tag;
+template <> struct Tag<float> {
+  using W = unsigned;
+  static __device__ __forceinline__ W make(float v, unsigned e) { return __float_as_uint(v) | ((e & 1u) << 31); }
+  static __device__ __forceinline__ bool ok(W w, unsigned e) { return (w >> 31) == (e & 1u); }
+  static __device__ __forceinline__ float val(W w) { return __uint_as_float(w & 0x7fffffffu); }
+  static __device__ __forceinline__ W ld(const float* p) { return ld_w(reinterpret_cast<const unsigned*>(p)); }
+  static __device__ __forceinline__ void st(float* p, float v, unsigned e) { st_w(reinterpret_cast<unsigned*>(p), make(v, e)); }
+  static __device__ __forceinline__ void st4(float* p, const float* v, unsigned e) {
+    st_w4(reinterpret_cast<unsigned*>(p), make_uint4(make(v[0], e), make(v[1], e), make(v[2], e), make(v[3], e)));
+  }
+};
+template <> struct Tag<double> {
+  using W = uint64_t;
+  static __device__ __forceinline__ W make(double v, unsigned e) {
+    return (uint64_t)__double_as_longlong(v) | ((uint64_t)(e & 1u) << 63);
+  }
+  static __device__ __forceinline__ bool ok(W w, unsigned e) { return (unsigned)(w >> 63) == (e & 1u); }
+  static __device__ __forceinline__ double val(W w) { return __longlong_as_double((long long)(w & 0x7fffffffffffffffull)); }
+  static __device__ __forceinline__ W ld(const double* p) { return ld_tag(reinterpret_cast<const uint64_t*>(p)); }
+  static __device__ __forceinline__ void st(double* p, double v, unsigned e) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(make(v, e)) : "memory");
+  }
+  static __device__ __forceinline__ void st4(double* p, const double* v, unsigned e) {   // 2 words (double2)
+    asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(make(v[0], e)), "l"(make(v[1], e))
+                 : "memory");
+  }
+};
 
 template <typename T> struct VecT;
 template <> struct VecT<float>  { using t = float4;  static constexpr int W = 4; };
@@ -76,36 +111,66 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
   // vector index of slot k for this lane: q = (cg·VPL + k)·32 + lane
   auto qidx = [&](int k) -> long { return ((long)cg * VPL + k) * 32 + lane; };
 
-  // ---------------- column-slice reduction + S (after barrier 1) ----------------
-  auto reduce_columns_and_S = [&]() {
+  // S/n, S/n² and c/n without full FP64 divisions: r = RN(1/d), then q + r·(x − q·d) = RN(x/d)
+  // (Markstein; see K4r and tools/div_probe.cu)
+  const double rn = __drcp_rn(dn), rnn = __drcp_rn(nn);
+  auto div_n = [&](double x, double d, double r) {
+    const double q = x * r;
+    return fma(r, fma(-q, d, x), q);
+  };
+  using TG = Tag<T>;
+  // ---------------- column-slice reduction + S of epoch e ----------------
+  // CTA b sums column slice b over all CTAs' tagged partials (warp ↔ source CTA k ≡ warp mod 16,
+  // all loads in flight, then re-read until tagged e; FP64 in CTA order, warps combined in order)
+  // and publishes c (tagged e); warp 0 collects S from the per-CTA masses (tagged, parity buffer).
+  constexpr int NI = (32 * 5 + kSdsnWarps - 1) / kSdsnWarps;   // G ≤ 160 sources
+  auto reduce_columns_and_S = [&](unsigned e) {
     const long cb = (long)b * n / G, ce = (long)(b + 1) * n / G;
     for (long c0 = cb; c0 < ce; c0 += 32) {
       const long col = c0 + lane;
       double acc = 0.0;
-      if (col < ce)
-        for (unsigned k = warp; k < G; k += kSdsnWarps) acc += (double)ldcg(colpart + (long)k * ld + col);
+      if (col < ce) {
+        typename TG::W w[NI];
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+          const unsigned k = warp + i * kSdsnWarps;
+          w[i] = k < G ? TG::ld(colpart + (long)k * ld + col) : TG::make((T)0, e);
+        }
+        bool ok;
+        do {
+          ok = true;
+#pragma unroll
+          for (int i = 0; i < NI; ++i)
+            if (!TG::ok(w[i], e)) { ok = false; w[i] = TG::ld(colpart + (long)(warp + i * kSdsnWarps) * ld + col); }
+        } while (!ok);
+#pragma unroll
+        for (int i = 0; i < NI; ++i) acc += (double)TG::val(w[i]);
+      }
       s_red[warp][lane] = acc;
       __syncthreads();
       if (tid < 32 && c0 + tid < ce) {
-        double s = 0.0;
+        double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < kSdsnWarps; ++w) s += s_red[w][tid];
-        P.cvec[c0 + tid] = s;
+        for (int w = 0; w < kSdsnWarps; ++w) sum += s_red[w][tid];
+        Tag<double>::st(P.cvec + c0 + tid, sum, e);
       }
       __syncthreads();
     }
     if (warp == 0) {
-      double s = 0.0;
-      for (unsigned k = lane; k < G; k += 32) s += ldcg(P.Spart + k);
-      s = warp_sum_d(s);
-      if (lane == 0) s_scal[0] = s;
+      double v[5];
+      wait_d1_lanes<5>(reinterpret_cast<const uint64_t*>(P.Spart) + (size_t)(e & 1) * G, (int)G, lane, (e >> 1) & 1u, v);
+      double sum = 0.0;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) sum += v[i];
+      sum = warp_sum_d(sum);
+      if (lane == 0) s_scal[0] = sum;
     }
   };
 
   // ---------------- one sweep over the CTA's rows ----------------
   // MODE SCALE: y ← fl(s·y) (written only if P.scale); MODE PASS: y ← max(0, (y + a_i) + b_j).
   // Both accumulate the row sums (s_r) and column partials (colpart[b]) of the new values.
-  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W]) {
+  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W], unsigned e) {
     constexpr int mode = decltype(mode_c)::value;
     T colacc[VPL][W];
 #pragma unroll
@@ -179,12 +244,14 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     };
     if (full) run(std::true_type{});
     else run(std::false_type{});
-    // column partials of this CTA → colpart[b]
+    // column partials of this CTA → colpart[b] (tagged e; e = 0: last pass, nothing published)
     if (RG == 1) {
+      if (e != 0) {
 #pragma unroll
-      for (int k = 0; k < VPL; ++k) {
-        const long q = qidx(k);
-        if (q < nvec) reinterpret_cast<VT*>(colpart + (long)b * ld)[q] = vmake<T>(colacc[k]);
+        for (int k = 0; k < VPL; ++k) {
+          const long q = qidx(k);
+          if (q < nvec) TG::st4(colpart + (long)b * ld + q * W, colacc[k], e);
+        }
       }
       __syncthreads();
     } else {
@@ -194,30 +261,32 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
         if (q < nvec) reinterpret_cast<VT*>(s_colstage + (long)rg * ld)[q] = vmake<T>(colacc[k]);
       }
       __syncthreads();
-      for (long q = tid; q < nvec; q += kSdsnThreads) {
-        T acc[W];
-        vget<T>(reinterpret_cast<const VT*>(s_colstage)[q], acc);
-        for (int g = 1; g < RG; ++g) {
-          T e[W];
-          vget<T>(reinterpret_cast<const VT*>(s_colstage + (long)g * ld)[q], e);
+      if (e != 0) {
+        for (long q = tid; q < nvec; q += kSdsnThreads) {
+          T acc[W];
+          vget<T>(reinterpret_cast<const VT*>(s_colstage)[q], acc);
+          for (int g = 1; g < RG; ++g) {
+            T x[W];
+            vget<T>(reinterpret_cast<const VT*>(s_colstage + (long)g * ld)[q], x);
 #pragma unroll
-          for (int w = 0; w < W; ++w) acc[w] += e[w];
+            for (int w = 0; w < W; ++w) acc[w] += x[w];
+          }
+          TG::st4(colpart + (long)b * ld + q * W, acc, e);
         }
-        reinterpret_cast<VT*>(colpart + (long)b * ld)[q] = vmake<T>(acc);
       }
     }
-    // row sums (fixed order over column groups) and the CTA's mass partial
+    // row sums (fixed order over column groups) and the CTA's mass partial (tagged, parity buffer)
     for (int i = tid; i < R; i += kSdsnThreads) {
       double s = 0.0;
       for (int g = 0; g < CG; ++g) s += s_rowpart[i * CG + g];
       s_r[i] = s;
     }
     __syncthreads();
-    if (warp == 0) {
+    if (warp == 0 && e != 0) {
       double s = 0.0;
       for (int i = lane; i < R; i += 32) s += s_r[i];
       s = warp_sum_d(s);
-      if (lane == 0) P.Spart[b] = s;
+      if (lane == 0) st_d1(reinterpret_cast<uint64_t*>(P.Spart) + (size_t)(e & 1) * G + b, s, (e >> 1) & 1u);
     }
   };
 
@@ -245,12 +314,14 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     if (tid == 0) {
       double mm = 0.0;
       for (int w = 0; w < kSdsnWarps; ++w) mm = fmax(mm, s_red[w][0]);
-      P.Mpart[b] = mm;
+      st_d1(reinterpret_cast<uint64_t*>(P.Mpart) + b, mm, 1u);
     }
-    grid_barrier(P.bar, G);
     if (warp == 0) {
+      double v[5];
+      wait_d1_lanes<5>(reinterpret_cast<const uint64_t*>(P.Mpart), (int)G, lane, 1u, v);
       double mm = 0.0;
-      for (unsigned k = lane; k < G; k += 32) mm = fmax(mm, ldcg(P.Mpart + k));
+#pragma unroll
+      for (int i = 0; i < 5; ++i) mm = fmax(mm, v[i]);
       mm = warp_max_d(mm);
       if (lane == 0) s_scal[1] = mm;
     }
@@ -283,37 +354,53 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     for (int k = 0; k < VPL; ++k)
 #pragma unroll
       for (int w = 0; w < W; ++w) bz[k][w] = (T)0;
-    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz);
+    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz, 1u);
   }
-  grid_barrier(P.bar, G);
-  reduce_columns_and_S();
-  grid_barrier(P.bar, G);
+  unsigned ep = 1;                                   // epoch of the current exchange
+  reduce_columns_and_S(ep);
 
   // ---------------- pass loop ----------------
   int j = 0;
   double gam = 0.0;
   for (;; ++j) {
+    T bv[VPL][W];                                     // b for this lane's columns: −c/n of epoch ep
+    {
+      typename Tag<double>::W cw[VPL][W];
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const long col = qidx(k) * W + w;
+          cw[k][w] = col < n ? Tag<double>::ld(P.cvec + col) : Tag<double>::make(0.0, ep);
+        }
+      bool ok;
+      do {
+        ok = true;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+#pragma unroll
+          for (int w = 0; w < W; ++w)
+            if (!Tag<double>::ok(cw[k][w], ep)) { ok = false; cw[k][w] = Tag<double>::ld(P.cvec + qidx(k) * W + w); }
+      } while (!ok);
+#pragma unroll
+      for (int k = 0; k < VPL; ++k)
+#pragma unroll
+        for (int w = 0; w < W; ++w)
+          bv[k][w] = (qidx(k) * W + w < n) ? (T)(-div_n(Tag<double>::val(cw[k][w]), dn, rn)) : (T)0;
+    }
+    __syncthreads();                                  // s_scal[0] (S of epoch ep) from the reduction
     const double S = s_scal[0];
-    gam = S / dn - 1.0;                                                // γ_j
+    gam = div_n(S, dn, rn) - 1.0;                                      // γ_j = S/n − 1
     if (b == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[j] = gam;
     const bool last = P.sdsn_fixed > 0 ? (j + 1 >= P.sdsn_fixed)
                                        : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
-    const double abase = 1.0 / dn + S / nn;
-    for (int i = tid; i < R; i += kSdsnThreads) s_a[i] = (T)(abase - s_r[i] / dn);
-    T bv[VPL][W];                                                      // b for this lane's columns
-#pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      const long q = qidx(k);
-#pragma unroll
-      for (int w = 0; w < W; ++w)
-        bv[k][w] = (q * W + w < n) ? (T)(-ldcg(P.cvec + q * W + w) / dn) : (T)0;
-    }
+    const double abase = rn + div_n(S, nn, rnn);                       // 1/n + S/n²
+    for (int i = tid; i < R; i += kSdsnThreads) s_a[i] = (T)(abase - div_n(s_r[i], dn, rn));
     __syncthreads();
-    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv);
+    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv, last ? 0u : ep + 1);
     if (last) break;
-    grid_barrier(P.bar, G);
-    reduce_columns_and_S();
-    grid_barrier(P.bar, G);
+    ++ep;
+    reduce_columns_and_S(ep);
   }
   if (b == 0 && tid == 0) {
     *P.passes_out = j + 1;
@@ -369,8 +456,17 @@ cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_
   int vpl, cg;
   if (!plan(p.n, f64, &vpl, &cg)) return cudaErrorInvalidValue;
   const int grid = sdsn_grid_for(p.n, num_sms);
+  if (grid > 160) return cudaErrorInvalidValue;          // the tagged reductions cover ≤ 160 CTAs
   if (grid_out) *grid_out = grid;
-  cudaError_t e = cudaMemsetAsync(p.bar, 0, 2 * sizeof(unsigned), st);
+  // tagged exchange words start "not ready" for every epoch's first read: colpart, cvec and Mpart
+  // zero (tag 0 ≠ epoch 1), Spart buffer 1 (epoch 1, tag 0) set to tag 1, buffer 0 (epoch 2, tag 1)
+  // zero.  Spart and Mpart hold 2·grid and grid words.
+  const size_t ts = f64 ? 8 : 4;
+  cudaError_t e = cudaMemsetAsync(p.colpart, 0, (size_t)grid * p.ld * ts, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.cvec, 0, (size_t)p.ld * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.Mpart, 0, (size_t)grid * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.Spart, 0, (size_t)grid * 8, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p.Spart + grid, 0x80, (size_t)grid * 8, st);
   if (e != cudaSuccess) return e;
   if (f64) {
     switch (vpl) {
