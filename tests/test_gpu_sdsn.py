@@ -150,3 +150,31 @@ def test_sdsn_fp32_onchip_sizes(n):
     tol = 16 * k * U32 * 5.0
     assert np.max(np.abs(D.cpu().numpy().astype(np.float64) - Dr)) <= tol
     assert np.max(np.abs(np.array(gam[:k]) - np.array(go[:k]))) <= 1e-4
+
+
+@pytest.mark.parametrize("n", [4100, 6000])
+def test_sdsn_fp32_streaming_parity(n):
+    # FP32 above the on-chip limit (n > 4096) runs the streaming kernel K4 (tagged exchange, no grid
+    # barriers); ragged row blocks and column tails; same tolerance model as the on-chip sizes.
+    X = random_nonneg(_rng(77 + n), n, "sparse").astype(np.float32)
+    X[0, 0] = max(X[0, 0], 0.5)
+    k = 6
+    h = fram_create(n, schedule=Schedule(theta=10.0, sdsn_fixed=k))
+    D, kk, gam = fram_sdsn(h, _gpu(X, torch.float32), "fp32")
+    assert kk == k
+    Dr, _, go = oracle.sdsn(X.astype(np.float64), 10.0, sdsn_fixed=k, return_gammas=True)
+    tol = 16 * k * U32 * 5.0
+    assert np.max(np.abs(D.cpu().numpy().astype(np.float64) - Dr)) <= tol
+    assert np.max(np.abs(np.array(gam[:k]) - np.array(go[:k]))) <= 1e-4
+
+
+def test_sdsn_fp32_streaming_gamma_stop():
+    # γ-test stop on the streaming FP32 path: pass count within the near-threshold slack of the oracle's
+    n = 4224
+    X = random_nonneg(_rng(4224), n, "uniform").astype(np.float32)
+    h = fram_create(n, schedule=Schedule(theta=2.0, gamma_th=1e-2, sdsn_max=200))
+    D, k, gam = fram_sdsn(h, _gpu(X, torch.float32), "fp32")
+    _, ko, _ = oracle.sdsn(X.astype(np.float64), 2.0, 1e-2, 200, return_gammas=True)
+    assert abs(k - ko) <= max(2, 0.02 * ko)
+    Dn = D.cpu().numpy().astype(np.float64)
+    assert np.all(Dn >= 0.0)
