@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
   // ---------------- one sweep over the CTA's rows ----------------
   // MODE SCALE: y ← fl(s·y) (written only if P.scale); MODE PASS: y ← max(0, (y + a_i) + b_j).
   // Both accumulate the row sums (s_r) and column partials (colpart[b]) of the new values.
-  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W], unsigned e) {
+  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W], unsigned e, bool rev) {
     constexpr int mode = decltype(mode_c)::value;
     T colacc[VPL][W];
 #pragma unroll
@@ -187,8 +187,11 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       kind[k] = qv[k] >= (int)nvec ? 0 : ((qv[k] + 1) * W <= (int)n ? 1 : 2);
     }
     VT buf[PD][VPL];
+    // rev: the rows in reverse order (odd passes), so a pass starts on the rows the previous pass
+    // wrote last — still in L2 when the iterate is about the L2 size (FP64 at n = 4096)
+    auto rmap = [&](int rr) { return rev ? nrw - 1 - rr : rr; };
     auto load_row = [&](int s, int rr) {
-      const VT* row = Yc + (rg + rr * RG) * ldv;
+      const VT* row = Yc + (rg + rmap(rr) * RG) * ldv;
 #pragma unroll
       for (int k = 0; k < VPL; ++k)
         if (kind[k]) buf[s][k] = __ldcg(row + qv[k]);
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
           rs[s] = (T)0;
           const int rr = base + s;
           if (rr < nrw) {
-            const int il = rg + rr * RG;                     // local row index
+            const int il = rg + rmap(rr) * RG;               // local row index
             VT* row = Yc + il * ldv;
             const T a = (mode == SWEEP_PASS) ? s_a[il] : (T)0;
 #pragma unroll
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
         if (lane == 0) {
 #pragma unroll
           for (int s = 0; s < PD; ++s)
-            if (base + s < nrw) s_rowpart[(rg + (base + s) * RG) * CG + cg] = (double)rs[s];
+            if (base + s < nrw) s_rowpart[(rg + rmap(base + s) * RG) * CG + cg] = (double)rs[s];
         }
       }
     };
@@ -354,7 +357,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     for (int k = 0; k < VPL; ++k)
 #pragma unroll
       for (int w = 0; w < W; ++w) bz[k][w] = (T)0;
-    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz, 1u);
+    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz, 1u, false);
   }
   unsigned ep = 1;                                   // epoch of the current exchange
   reduce_columns_and_S(ep);
@@ -397,7 +400,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     const double abase = rn + div_n(S, nn, rnn);                       // 1/n + S/n²
     for (int i = tid; i < R; i += kSdsnThreads) s_a[i] = (T)(abase - div_n(s_r[i], dn, rn));
     __syncthreads();
-    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv, last ? 0u : ep + 1);
+    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv, last ? 0u : ep + 1, (j & 1) == 0);
     if (last) break;
     ++ep;
     reduce_columns_and_S(ep);
