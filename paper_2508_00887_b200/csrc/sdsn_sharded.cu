@@ -106,7 +106,11 @@ __global__ void __launch_bounds__(kShThreads) sh_pass_kernel(ShardSdsnParams P, 
   __syncthreads();
   // row partials per warp in shared memory (no barrier per row); combined once after the sweep
   double* s_rp = reinterpret_cast<double*>(BS ? s_b + ld : s_col + ld);   // [rows of this CTA][warps]
-  for (long i = r0; i < r1; ++i) {
+  // odd passes walk the rows in reverse ("snake" order): a pass starts on the rows the previous one
+  // wrote last, which are still in L2 when the row block is about the L2 size (K4 does the same)
+  const bool rev = mode == 1 && (p & 1);
+  for (long ii = r0; ii < r1; ++ii) {
+    const long i = rev ? r0 + r1 - 1 - ii : ii;
     VT* row = reinterpret_cast<VT*>(Y + i * ld);
     const T a = mode ? (T)(abase - P.rsum[i] / dn) : (T)0;      // R9: a_i in FP64, rounded
     double rs = 0.0;
