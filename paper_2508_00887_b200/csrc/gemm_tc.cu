@@ -9,6 +9,8 @@
 //   GEMM2 (epi 1): Aop = A',  Bop = Uᵀ   → D = A'·U, stored as G = D + λK' in FP32.
 // Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one elected lane), w2 TMEM allocator,
 // w4-w7 epilogue (TMEM lane quarter = warp % 4).  Tile 128×256×(128 B of K), 4-stage mbarrier ring.
+// Persistent: one CTA per SM walks the tiles t = blockIdx.x, +gridDim.x, …; the accumulator is
+// double-buffered in TMEM (2 × 256 columns), so the epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 #include "common.cuh"
 #include "internal.h"
@@ -21,7 +23,7 @@ constexpr int TILE_A = BM * 128;            // bytes: 128 rows × 128 B
 constexpr int TILE_B = BN * 128;            // bytes: 256 rows × 128 B
 constexpr int STAGE_BYTES = TILE_A + TILE_B;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
-constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t TMEM_COLS = 512;                 // two 128×256 FP32 accumulators
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -133,16 +135,18 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint8_t* sB = smem + STAGES * TILE_A;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + STAGES;                    // [2] accumulator b ready (MMA → epilogue)
+  uint64_t* tempty = tfull + 2;                        // [2] accumulator b drained (epilogue → MMA)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (int)((ea.K + BK - 1) / BK);
+  const int ntn = (int)((ea.N + BN - 1) / BN), ntm = (int)((ea.M + BM - 1) / BM);
+  const int ntiles = ntm * ntn;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(full + s, 1); mbar_init(empty + s, 1); }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) { mbar_init(tfull + b, 1); mbar_init(tempty + b, 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -158,80 +162,100 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
-    if (lane == 0) {                                   // ---- TMA producer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-        mbar_wait(empty + s, ph ^ 1u);
-        mbar_expect_tx(full + s, STAGE_BYTES);
-        tma_load_2d(&tmA, full + s, sA + s * TILE_A, kb * BK, m0);
-        if (ea.kchunk > 0) {
-          const long k0 = (long)kb * BK;
-          tma_load_3d(&tmB, full + s, sB + s * TILE_B, (int)(k0 % ea.kchunk), n0, (int)(k0 / ea.kchunk));
-        } else {
-          tma_load_2d(&tmB, full + s, sB + s * TILE_B, kb * BK, n0);
+    if (lane == 0) {                                   // ---- TMA producer (ring continues across tiles)
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int m0 = (tile / ntn) * BM, n0 = (tile % ntn) * BN;
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+          mbar_wait(empty + s, ph ^ 1u);
+          mbar_expect_tx(full + s, STAGE_BYTES);
+          tma_load_2d(&tmA, full + s, sA + s * TILE_A, kb * BK, m0);
+          if (ea.kchunk > 0) {
+            const long k0 = (long)kb * BK;
+            tma_load_3d(&tmB, full + s, sB + s * TILE_B, (int)(k0 % ea.kchunk), n0, (int)(k0 / ea.kchunk));
+          } else {
+            tma_load_2d(&tmB, full + s, sB + s * TILE_B, kb * BK, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {                                   // ---- MMA issuer
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
-        mbar_wait(full + s, ph);
+      int it = 0, ti = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+        const int b = ti & 1;
+        const uint32_t use = (uint32_t)(ti >> 1) & 1u;
+        mbar_wait(tempty + b, use ^ 1u);               // accumulator b drained by the epilogue
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + s * TILE_A), b0 = smem_u32(sB + s * TILE_B);
+        const uint32_t acc = tmem + (uint32_t)(b * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES;
+          const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + s * TILE_A), b0 = smem_u32(sB + s * TILE_B);
 #pragma unroll
-        for (int k = 0; k < BK / UK; ++k)
-          umma<OP>(tmem, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), IDESC, (kb | k) != 0 ? 1u : 0u);
-        umma_commit(empty + s);                        // frees the SMEM slot when these MMAs finish
+          for (int k = 0; k < BK / UK; ++k)
+            umma<OP>(acc, sdesc_sw128(a0 + k * 32), sdesc_sw128(b0 + k * 32), IDESC, (kb | k) != 0 ? 1u : 0u);
+          umma_commit(empty + s);                      // frees the SMEM slot when these MMAs finish
+        }
+        umma_commit(tfull + b);                        // accumulator b complete
       }
-      umma_commit(tfull);                              // accumulator complete
     }
   } else if (warp >= 4) {                              // ---- epilogue: TMEM → registers → HBM
     const int q = warp & 3;
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const long row = (long)m0 + q * 32 + lane;
+    int ti = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+      const int b = ti & 1;
+      const int m0 = (tile / ntn) * BM, n0 = (tile % ntn) * BN;
+      mbar_wait(tfull + b, (uint32_t)(ti >> 1) & 1u);
+      tc_fence_after();
+      const long row = (long)m0 + q * 32 + lane;
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
-      uint32_t v[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), v);
-      const long col0 = (long)n0 + c * 32;
-      if (row < ea.M && col0 < ea.N) {
-        if (ea.epi == 0) {
-          // transposed store: out[col][row]; lanes of a warp write consecutive rows (coalesced)
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c * 32), v);
+        const long col0 = (long)n0 + c * 32;
+        if (row < ea.M && col0 < ea.N) {
+          if (ea.epi == 0) {
+            // transposed store: out[col][row]; lanes of a warp write consecutive rows (coalesced)
 #pragma unroll
-          for (int jj = 0; jj < 32; ++jj) {
-            const long col = col0 + jj;
-            if (col < ea.N) OpStore<OP>::st(ea.out, col * ea.ldo + row, __uint_as_float(v[jj]));
-          }
-        } else {
-          float* g = reinterpret_cast<float*>(ea.out) + row * ea.ldo;
-          const float* kr = ea.Kq ? ea.Kq + row * ea.ldo : nullptr;
-          if (col0 + 32 <= ea.N) {
-#pragma unroll
-            for (int jj = 0; jj < 32; jj += 4) {
-              float4 o = make_float4(__uint_as_float(v[jj]), __uint_as_float(v[jj + 1]),
-                                     __uint_as_float(v[jj + 2]), __uint_as_float(v[jj + 3]));
-              if (kr) {
-                const float4 kk = *reinterpret_cast<const float4*>(kr + col0 + jj);
-                o.x += ea.lam * kk.x; o.y += ea.lam * kk.y; o.z += ea.lam * kk.z; o.w += ea.lam * kk.w;
-              }
-              *reinterpret_cast<float4*>(g + col0 + jj) = o;
-            }
-          } else {
             for (int jj = 0; jj < 32; ++jj) {
               const long col = col0 + jj;
-              if (col < ea.N) {
-                float o = __uint_as_float(v[jj]);
-                if (kr) o += ea.lam * kr[col];
-                g[col] = o;
+              if (col < ea.N) OpStore<OP>::st(ea.out, col * ea.ldo + row, __uint_as_float(v[jj]));
+            }
+          } else {
+            float* g = reinterpret_cast<float*>(ea.out) + row * ea.ldo;
+            const float* kr = ea.Kq ? ea.Kq + row * ea.ldo : nullptr;
+            if (col0 + 32 <= ea.N) {
+#pragma unroll
+              for (int jj = 0; jj < 32; jj += 4) {
+                float4 o = make_float4(__uint_as_float(v[jj]), __uint_as_float(v[jj + 1]),
+                                       __uint_as_float(v[jj + 2]), __uint_as_float(v[jj + 3]));
+                if (kr) {
+                  const float4 kk = *reinterpret_cast<const float4*>(kr + col0 + jj);
+                  o.x += ea.lam * kk.x; o.y += ea.lam * kk.y; o.z += ea.lam * kk.z; o.w += ea.lam * kk.w;
+                }
+                *reinterpret_cast<float4*>(g + col0 + jj) = o;
+              }
+            } else {
+              for (int jj = 0; jj < 32; ++jj) {
+                const long col = col0 + jj;
+                if (col < ea.N) {
+                  float o = __uint_as_float(v[jj]);
+                  if (kr) o += ea.lam * kr[col];
+                  g[col] = o;
+                }
               }
             }
           }
         }
       }
+      tc_fence_before();                               // this warp's TMEM reads of buffer b are done
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty + b)) : "memory");
     }
   }
   tc_fence_before();
@@ -302,8 +326,14 @@ cudaError_t launch_op(const GemmArgs& g, cudaStream_t st) {
   auto fn = gemm_tc_kernel<OP>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
   if (e != cudaSuccess) return e;
-  dim3 grid((unsigned)((g.N + BN - 1) / BN), (unsigned)((g.M + BM - 1) / BM));
-  fn<<<grid, GEMM_THREADS, SMEM_BYTES, st>>>(ta, tb, ea);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long tiles = ((g.N + BN - 1) / BN) * ((g.M + BM - 1) / BM);
+  fn<<<(unsigned)(tiles < nsm ? tiles : nsm), GEMM_THREADS, SMEM_BYTES, st>>>(ta, tb, ea);
   return cudaGetLastError();
 }
 
