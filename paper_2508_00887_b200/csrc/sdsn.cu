@@ -21,10 +21,12 @@
 // are non-negative) and is re-read until the tag matches (the K4r exchange, xchg.cuh).
 // Algorithmic bytes per pass: 8n² (FP32) / 16n² (FP64) of Y, + O(G·n) of partials.
 #include <stdlib.h>
+#include <algorithm>
 #include <type_traits>
 #include "common.cuh"
 #include "internal.h"
 #include "xchg.cuh"
+#include "tmem_ldst.cuh"
 
 namespace fram {
 
@@ -64,6 +66,9 @@ template <typename T> struct VecT;
 template <> struct VecT<float>  { using t = float4;  static constexpr int W = 4; };
 template <> struct VecT<double> { using t = double2; static constexpr int W = 2; };
 
+#ifndef SDSN_ONCHIP
+#define SDSN_ONCHIP 1
+#endif
 constexpr int kSdsnThreads = 512;
 constexpr int kSdsnWarps = kSdsnThreads / 32;
 constexpr int kSdsnMaxRows = 1024;
@@ -83,14 +88,21 @@ __device__ __forceinline__ double warp_sum_t(double v) { return warp_sum_d(v); }
 enum { SWEEP_SCALE = 0, SWEEP_PASS = 1 };
 
 template <typename T, int VPL>
-__global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int CG) {
+__global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int CG, int NT, int NSM) {
   using VT = typename VecT<T>::t;
   constexpr int W = VecT<T>::W;
   constexpr int PD = VPL >= 8 ? 1 : 16 / VPL;                // rows in flight per warp
+  constexpr int WPR = VPL * (int)sizeof(VT) / 4;             // 32-bit words per thread per row
   extern __shared__ __align__(16) unsigned char dsm[];
   const long rows_max = (P.n + gridDim.x - 1) / gridDim.x + 1;
   double* s_rowpart = reinterpret_cast<double*>(dsm);       // [rows_max][CG]
   T* s_colstage = reinterpret_cast<T*>(dsm + ((sizeof(double) * rows_max * CG + 15) & ~15ul));   // [RG][ld]
+  // On-chip rows (RG = 1 only, NT + NSM > 0): a warp's first NT rows live in TMEM (lane quarter
+  // warp%4, column block (row·4 + warp/4)·WPR), the next NSM rows in shared memory, the rest stream
+  // through L2/HBM.  A pass then moves only the streamed rows through the memory system (FP64 at
+  // n = 4096: about half of the 128 MB iterate, which then fits in L2).
+  VT* s_on = reinterpret_cast<VT*>(s_colstage);              // [NSM][nvec] (RG = 1: no column staging)
+  __shared__ uint32_t s_tmem;
   __shared__ double s_r[kSdsnMaxRows];
   __shared__ T s_a[kSdsnMaxRows];
   __shared__ double s_red[kSdsnWarps][32];
@@ -104,6 +116,24 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
   const long r0 = (long)b * n / G, r1 = (long)(b + 1) * n / G;
   const int R = (int)(r1 - r0);
   const long nvec = (n + W - 1) / W;
+  if (NT > 0) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&s_tmem)), "r"(512));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
+  const uint32_t tmem = NT > 0 ? s_tmem + ((uint32_t)((warp & 3) * 32) << 16) : 0u;
+  auto tmem_free = [&]() {
+    if (NT > 0) {
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(s_tmem), "r"(512));
+    }
+  };
   const int nrw = (R > rg) ? (R - rg + RG - 1) / RG : 0;     // rows handled by this warp
   T* Y = reinterpret_cast<T*>(P.Y);
   T* colpart = reinterpret_cast<T*>(P.colpart);
@@ -170,7 +200,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
   // ---------------- one sweep over the CTA's rows ----------------
   // MODE SCALE: y ← fl(s·y) (written only if P.scale); MODE PASS: y ← max(0, (y + a_i) + b_j).
   // Both accumulate the row sums (s_r) and column partials (colpart[b]) of the new values.
-  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W], unsigned e, bool rev) {
+  auto sweep = [&](auto mode_c, double sc, const T (&bv)[VPL][W], unsigned e, bool rev, bool wb) {
     constexpr int mode = decltype(mode_c)::value;
     T colacc[VPL][W];
 #pragma unroll
@@ -187,9 +217,12 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       kind[k] = qv[k] >= (int)nvec ? 0 : ((qv[k] + 1) * W <= (int)n ? 1 : 2);
     }
     VT buf[PD][VPL];
-    // rev: the rows in reverse order (odd passes), so a pass starts on the rows the previous pass
-    // wrote last — still in L2 when the iterate is about the L2 size (FP64 at n = 4096)
-    auto rmap = [&](int rr) { return rev ? nrw - 1 - rr : rr; };
+    // on-chip rows first (local rows [0, non)), then the streamed rows with the register ring.
+    // rev: the streamed rows in reverse order (odd passes), so a pass starts on the rows the
+    // previous pass wrote last — still in L2 when they are about the L2 size
+    const int non = RG == 1 ? min(NT + NSM, nrw) : 0;
+    const int nrs = nrw - non;
+    auto rmap = [&](int rr) { return non + (rev ? nrs - 1 - rr : rr); };
     auto load_row = [&](int s, int rr) {
       const VT* row = Yc + (rg + rmap(rr) * RG) * ldv;
 #pragma unroll
@@ -200,18 +233,63 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
 #pragma unroll
     for (int k = 0; k < VPL; ++k) full = full && (kind[k] == 1);
     full = __all_sync(0xffffffffu, full);
+    // the first streamed rows' loads are in flight while the on-chip rows are processed
 #pragma unroll
     for (int s = 0; s < PD; ++s)
-      if (s < nrw) load_row(s, s);
+      if (s < nrs) load_row(s, s);
+    // on-chip rows: one at a time (TMEM or shared memory; the scale sweep reads X from global)
+    for (int il = 0; il < non; ++il) {
+      // one register array holds the row slice: TMEM words, shared-memory or global vectors
+      uint32_t wv[WPR];
+      VT* row = Yc + il * ldv;
+      auto vec = [&](int k) -> VT& { return *reinterpret_cast<VT*>(&wv[k * (WPR / VPL)]); };
+      if (mode_c.value == SWEEP_SCALE) {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (kind[k]) vec(k) = __ldcg(row + qv[k]);
+      } else if (il < NT) {
+        tmem_ld<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
+        tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (kind[k]) vec(k) = s_on[(long)(il - NT) * nvec + qv[k]];
+      }
+      const T a = (mode_c.value == SWEEP_PASS) ? s_a[il] : (T)0;
+      T r = (T)0;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        if (kind[k]) {
+          T x[W];
+          vget<T>(vec(k), x);
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            T y;
+            if constexpr (decltype(mode_c)::value == SWEEP_PASS) y = tmax0((x[w] + a) + bv[k][w]);
+            else y = P.scale ? (T)(sc * (double)x[w]) : x[w];
+            if (kind[k] == 2 && qv[k] * W + w >= (int)n) y = (T)0;
+            x[w] = y;
+            r += y;
+            colacc[k][w] += y;
+          }
+          vec(k) = vmake<T>(x);
+          if (il >= NT) s_on[(long)(il - NT) * nvec + qv[k]] = vec(k);
+          if (wb) __stcg(row + qv[k], vec(k));
+        }
+      }
+      if (il < NT) tmem_st<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
+      r = warp_sum_t(r);
+      if (lane == 0) s_rowpart[il * CG + cg] = (double)r;
+    }
     auto run = [&](auto full_c) {
       constexpr bool FULL = decltype(full_c)::value;
-      for (int base = 0; base < nrw; base += PD) {
+      for (int base = 0; base < nrs; base += PD) {
         T rs[PD];
 #pragma unroll
         for (int s = 0; s < PD; ++s) {
           rs[s] = (T)0;
           const int rr = base + s;
-          if (rr < nrw) {
+          if (rr < nrs) {
             const int il = rg + rmap(rr) * RG;               // local row index
             VT* row = Yc + il * ldv;
             const T a = (mode == SWEEP_PASS) ? s_a[il] : (T)0;
@@ -233,7 +311,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
                 if (mode == SWEEP_PASS || P.scale) __stcg(row + qv[k], vmake<T>(e));
               }
             }
-            if (rr + PD < nrw) load_row(s, rr + PD);
+            if (rr + PD < nrs) load_row(s, rr + PD);
           }
         }
 #pragma unroll
@@ -241,12 +319,13 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
         if (lane == 0) {
 #pragma unroll
           for (int s = 0; s < PD; ++s)
-            if (base + s < nrw) s_rowpart[(rg + rmap(base + s) * RG) * CG + cg] = (double)rs[s];
+            if (base + s < nrs) s_rowpart[(rg + rmap(base + s) * RG) * CG + cg] = (double)rs[s];
         }
       }
     };
     if (full) run(std::true_type{});
     else run(std::false_type{});
+    if (NT > 0) tmem_wait_st();
     // column partials of this CTA → colpart[b] (tagged e; e = 0: last pass, nothing published)
     if (RG == 1) {
       if (e != 0) {
@@ -344,6 +423,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
         *P.passes_out = 0;
         P.sdsn_out[0] = 0.0; P.sdsn_out[1] = 0.0; P.sdsn_out[2] = 0.0;
       }
+      tmem_free();
       return;
     }
     sc = (P.theta / 2.0) / m;                         // R11: s = (θ/2)/max X, FP64
@@ -357,7 +437,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     for (int k = 0; k < VPL; ++k)
 #pragma unroll
       for (int w = 0; w < W; ++w) bz[k][w] = (T)0;
-    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz, 1u, false);
+    sweep(std::integral_constant<int, SWEEP_SCALE>{}, sc, bz, 1u, false, false);
   }
   unsigned ep = 1;                                   // epoch of the current exchange
   reduce_columns_and_S(ep);
@@ -400,7 +480,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     const double abase = rn + div_n(S, nn, rnn);                       // 1/n + S/n²
     for (int i = tid; i < R; i += kSdsnThreads) s_a[i] = (T)(abase - div_n(s_r[i], dn, rn));
     __syncthreads();
-    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv, last ? 0u : ep + 1, (j & 1) == 0);
+    sweep(std::integral_constant<int, SWEEP_PASS>{}, 1.0, bv, last ? 0u : ep + 1, (j & 1) == 0, last);
     if (last) break;
     ++ep;
     reduce_columns_and_S(ep);
@@ -410,6 +490,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     P.sdsn_out[0] = gam;
     P.sdsn_out[2] = s_scal[0];
   }
+  tmem_free();
 }
 
 // VPL (16-byte vectors per lane per row slice) and CG (column groups, CG·RG = 16 warps).
@@ -446,12 +527,25 @@ static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int 
   auto fn = sdsn_kernel<T, VPL>;
   const int RG = kSdsnWarps / cg;
   const long rows_max = (p.n + grid - 1) / grid + 1;
-  const size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0);
+  size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0);
+  // on-chip rows (one row group only): up to 128/WPR rows in TMEM and as many rows as fit in the
+  // shared memory that is left (227 KB opt-in minus the static arrays)
+  int nt = 0, nsm = 0;
+  if (RG == 1 && SDSN_ONCHIP) {
+    constexpr int WPR = VPL * (int)sizeof(typename VecT<T>::t) / 4;
+    const long R = (p.n + grid - 1) / grid;
+    nt = (int)std::min<long>(128 / WPR, R);
+    const long row_bytes = ((p.n + VecT<T>::W - 1) / VecT<T>::W) * (long)sizeof(typename VecT<T>::t);
+    const long stat = (long)(kSdsnMaxRows * (sizeof(double) + sizeof(T)) + kSdsnWarps * 32 * 8 + 256);
+    const long avail = 232448 - stat - (long)dsm;
+    nsm = (int)std::max<long>(0, std::min<long>(R - nt, avail / row_bytes));
+    dsm += (size_t)nsm * row_bytes;
+  }
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   if (e != cudaSuccess) return e;
   SdsnParams pp = p;
   int cgv = cg;
-  void* args[] = {&pp, &cgv};
+  void* args[] = {&pp, &cgv, &nt, &nsm};
   return cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kSdsnThreads), args, dsm, st);
 }
 
