@@ -32,15 +32,47 @@ __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict_
   __shared__ bool is_last;
   const double oma = 1.0 - alpha;
   double dd = 0.0, nn = 0.0;
+  auto upd1 = [&](double old, double d, double& nv) {
+    nv = __dadd_rn(__dmul_rn(oma, old), __dmul_rn(alpha, d));
+    const double df = __dsub_rn(nv, old);
+    dd = __fma_rn(df, df, dd);
+    nn = __fma_rn(nv, nv, nn);
+  };
+  const bool vec = (ld % 2 == 0);
+  const long npair = vec ? n / 2 : 0;                   // column pairs handled two-wide
   for (long i = blockIdx.x; i < rows; i += gridDim.x) {
     double* nr = N + i * ld;
     const TD* dr = D + i * ld;
-    for (long j = threadIdx.x; j < n; j += UPD_THREADS) {
-      const double old = nr[j];
-      const double nv = __dadd_rn(__dmul_rn(oma, old), __dmul_rn(alpha, (double)dr[j]));
-      const double df = __dsub_rn(nv, old);
-      dd = __fma_rn(df, df, dd);
-      nn = __fma_rn(nv, nv, nn);
+    // pairs of columns: 16-byte N and 8/16-byte D accesses, four pairs per thread in flight
+    constexpr int UNR = 4;
+    for (long p0 = threadIdx.x; p0 < npair; p0 += (long)UNR * UPD_THREADS) {
+      double2 o[UNR];
+      double d0[UNR], d1[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const long pp = p0 + (long)u * UPD_THREADS;
+        if (pp < npair) {
+          o[u] = reinterpret_cast<const double2*>(nr)[pp];
+          d0[u] = (double)dr[2 * pp];
+          d1[u] = (double)dr[2 * pp + 1];
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const long pp = p0 + (long)u * UPD_THREADS;
+        if (pp < npair) {
+          double2 nv;
+          upd1(o[u].x, d0[u], nv.x);
+          upd1(o[u].y, d1[u], nv.y);
+          reinterpret_cast<double2*>(nr)[pp] = nv;
+          store_op<OP>(Nq, i * ld + 2 * pp, nv.x);
+          store_op<OP>(Nq, i * ld + 2 * pp + 1, nv.y);
+        }
+      }
+    }
+    for (long j = 2 * npair + threadIdx.x; j < n; j += UPD_THREADS) {   // odd tail / odd ld
+      double nv;
+      upd1(nr[j], (double)dr[j], nv);
       nr[j] = nv;
       store_op<OP>(Nq, i * ld + j, nv);
     }
