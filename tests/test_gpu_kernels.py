@@ -73,6 +73,14 @@ def test_gradient_mixed(prec, n):
     assert np.max(np.abs(G.cpu().numpy() - Go)) <= 8 * uop * np.abs(Go).max()
 
 
+@pytest.mark.parametrize("prec", ["bf16", "tf32"])
+@pytest.mark.parametrize("n", [2500, 4096])
+def test_gradient_mixed_multi_tile(prec, n):
+    # more 128×256 tiles than SMs (200 and 512 tiles on 148 SMs): the persistent GEMM reuses both TMEM
+    # accumulator buffers and wraps the mbarrier phases; same bound as test_gradient_mixed
+    test_gradient_mixed(prec, n)
+
+
 def test_gradient_bf16_storage_input():
     # FRAM_DT_BF16 inputs (C5 stores A dense in BF16): same result as the FP64 copy of those values.
     n = 96
