@@ -235,13 +235,40 @@ fram_status gradient(fram_ctx* h, int op, bool haveK, cudaStream_t st) {
   return FRAM_OK;
 }
 
-bool use_resident(const fram_ctx* h, bool f64) {
+// SDSN kernel choice: 4 = K4c (one cluster; FP64 n ≤ ~600, FP32 n ≤ 32), 2 = K4r (FP32 on chip,
+// n ≤ 4096), 1 = K4 (streaming).  FRAM_SDSN_STREAM forces K4, FRAM_SDSN_NOCLUSTER skips K4c (dev
+// comparison of the kernels).
+int sdsn_kind(const fram_ctx* h, bool f64) {
   static const bool force_stream = getenv("FRAM_SDSN_STREAM") != nullptr;
-  return !f64 && !force_stream && fram::sdsn_res_grid(h->n, h->num_sms) > 0;
+  static const bool no_cluster = getenv("FRAM_SDSN_NOCLUSTER") != nullptr;
+  if (force_stream) return 1;
+  // K4c where it measured fastest (tools/sdsn_small_timing.py): FP64 up to its size limit (vs K4),
+  // FP32 only for n ≤ 32 (K4r is faster from n = 64 on)
+  if (!no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 32)) return 4;
+  if (!f64 && fram::sdsn_res_grid(h->n, h->num_sms) > 0) return 2;
+  return 1;
 }
+bool use_resident(const fram_ctx* h, bool f64) { return sdsn_kind(h, f64) == 2; }
 
 fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
   double* scal = h->scal.as<double>();
+  if (sdsn_kind(h, f64) == 4) {
+    fram::SdsnParams p{};
+    p.Y = h->Y.p;
+    p.n = h->n;
+    p.ld = h->ld;
+    p.theta = h->sched.theta;
+    p.gamma_th = h->sched.gamma_th;
+    p.sdsn_max = h->sched.sdsn_max;
+    p.sdsn_fixed = fixed;
+    p.scale = (h->sched.flags & FRAM_FLAG_NO_THETA_SCALE) ? 0 : 1;
+    p.passes_out = reinterpret_cast<int*>(scal + 8);
+    p.gamma_hist = h->ghist.as<double>();
+    p.sdsn_out = scal;
+    CK(fram::launch_sdsn_cluster(p, f64, st), "sdsn (cluster) launch");
+    h->launches += 1;
+    return FRAM_OK;
+  }
   if (use_resident(h, f64)) {
     fram::ResParams r{};
     r.Y = h->Y.as<float>();
@@ -672,7 +699,7 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     stats->sdsn_capped_calls = capped;
     stats->total_passes = total;
     stats->kernel_launches = h->launches;
-    stats->sdsn_kernel = use_resident(h, f64) ? 2 : 1;
+    stats->sdsn_kernel = sdsn_kind(h, f64);
     if (timing) {
       float a, b, cc;
       cudaEventElapsedTime(&a, h->ev[0], h->ev[1]);

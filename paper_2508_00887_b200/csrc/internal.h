@@ -22,6 +22,10 @@ struct SdsnParams {
 };
 // f64: T=double; else T=float.  Returns the grid used via *grid_out.
 cudaError_t launch_sdsn(const SdsnParams& p, bool f64, cudaStream_t st, int num_sms, int* grid_out);
+// K4c: small n on one thread-block cluster (≤ 16 CTAs), iterate in shared memory, DSMEM all-reduce;
+// uses Y, n, ld, theta, gamma_th, sdsn_max, sdsn_fixed, scale, passes_out, gamma_hist, sdsn_out only
+bool sdsn_cluster_supported(long n, bool f64);
+cudaError_t launch_sdsn_cluster(const SdsnParams& p, bool f64, cudaStream_t st);
 int sdsn_grid_for(long n, int num_sms);
 bool sdsn_supported(long n, bool f64);
 

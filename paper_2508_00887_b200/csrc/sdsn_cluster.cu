@@ -1,0 +1,272 @@
+// sdsn_cluster.cu — K4c: SDSN (Alg. 2) for small n on ONE thread-block cluster
+// of C ≤ 16 CTAs (one per SM).  The whole iterate stays in the CTAs' shared memory, and the per-pass
+// all-reduce of the column sums and the mass goes through distributed shared memory (DSMEM) with
+// two cluster barriers, instead of the L2 round trips that dominate K4/K4r when a pass has only
+// 20–800 columns (C1, C2).
+//
+// Same arithmetic as K4/K4r (readings R5, R9-R13): γ_j = S_j/n − 1 (lagged test),
+// a_i = (1/n + S/n²) − r_i/n and b_j = −c_j/n in FP64 rounded to T, y' = max(0, (y + a_i) + b_j); S/n,
+// S/n², r_i/n and c_j/n as RN(x/d) from a precomputed reciprocal and one FMA correction.
+//
+// CTA c owns rows [c·n/C, (c+1)·n/C) (R ≤ 64); warp w of the CTA sweeps rows w, w+8, …, lane l the
+// columns l, l+32, … (≤ 28 per lane).  Row sums: one warp per row (FP64 for T = double; FP32 per lane,
+// then FP64 for T = float).  Column sums: per-lane register partials → the 8 warps summed in order in
+// shared memory → CTA partial → DSMEM reduce-scatter: CTA k receives the partials of column slice k
+// from every CTA and sums them in CTA order (FP64) → b_j all-gathered into every CTA (DSMEM).  The
+// per-CTA masses are all-gathered the same way and summed in CTA order by every CTA, so γ and the
+// stop decision are identical everywhere.
+#include <math_constants.h>
+#include <algorithm>
+#include "common.cuh"
+#include "internal.h"
+
+namespace fram {
+namespace {
+
+constexpr int kCThreads = 256, kCWarps = 8, kCMaxCols = 28, kCMaxRows = 64, kCMaxCluster = 16;
+constexpr int kCColsPerThread = (32 * kCMaxCols + kCThreads - 1) / kCThreads;   // 4
+
+__device__ __forceinline__ uint32_t dsmem(const void* p, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void dst_f64(uint32_t a, double v) {
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ void dst_f32(uint32_t a, float v) {
+  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+template <typename T> __device__ __forceinline__ void dst_t(uint32_t a, T v);
+template <> __device__ __forceinline__ void dst_t<float>(uint32_t a, float v) { dst_f32(a, v); }
+template <> __device__ __forceinline__ void dst_t<double>(uint32_t a, double v) { dst_f64(a, v); }
+
+template <typename T>
+__global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P, int ldn) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  const int n = (int)P.n;
+  unsigned crank, csize;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank));
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(csize));
+  const int c = (int)crank, C = (int)csize;
+  const int r0 = (int)((long)c * n / C), r1 = (int)((long)(c + 1) * n / C), R = r1 - r0;
+  const int SL = (n + C - 1) / C;                        // ≥ every column slice
+  const int k0 = (int)((long)c * n / C), k1 = (int)((long)(c + 1) * n / C);   // my column slice
+  // the same layout in every CTA (DSMEM addresses are mapped from the local ones): sized by the
+  // largest row count, ceil(n/C)
+  const int Rmax = (n + C - 1) / C;
+  T* Ys = reinterpret_cast<T*>(dsm);                     // [Rmax][ldn] my rows
+  T* s_cp = Ys + (size_t)Rmax * ldn;                     // [8][ldn] per-warp column partials
+  T* s_recv = s_cp + (size_t)kCWarps * ldn;              // [C][SL] partials of my column slice
+  T* s_b = s_recv + (size_t)kCMaxCluster * SL;           // [ldn] b_j, all columns
+  __shared__ double s_Sp[kCMaxCluster];                  // per-CTA masses (all-gathered)
+  __shared__ double s_M[kCMaxCluster];                   // per-CTA maxima (all-gathered)
+  __shared__ double s_r[kCMaxRows], s_rn[kCMaxRows];     // row sums and r_i/n of my rows
+  __shared__ T s_a[kCMaxRows];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double dn = (double)n, nn = dn * dn;
+  const double rn = __drcp_rn(dn), rnn = __drcp_rn(nn);
+  auto div_n = [&](double x, double d, double r) {
+    const double q = x * r;
+    return fma(r, fma(-q, d, x), q);
+  };
+  const T* X = reinterpret_cast<const T*>(P.Y);
+
+  // ---- load my rows and their max (Alg.2 step 1), max all-gathered through DSMEM ----
+  double lmax = 0.0;
+  for (int i = warp; i < R; i += kCWarps)
+    for (int j = lane; j < n; j += 32) {
+      const T x = X[(long)(r0 + i) * P.ld + j];
+      Ys[i * ldn + j] = x;
+      lmax = fmax(lmax, (double)x);
+    }
+  lmax = warp_max_d(lmax);
+  __shared__ double s_w[kCWarps];
+  if (lane == 0) s_w[warp] = lmax;
+  __syncthreads();
+  if (tid < C) {
+    double m = 0.0;
+    for (int w = 0; w < kCWarps; ++w) m = fmax(m, s_w[w]);
+    dst_f64(dsmem(&s_M[c], (unsigned)tid), m);           // my max into CTA tid's s_M[c]
+  }
+  cluster_sync();
+  double m = 0.0;
+  for (int k = 0; k < C; ++k) m = fmax(m, s_M[k]);
+  if (m == 0.0) {                                        // R10: all-zero ⇒ 11ᵀ/n, 0 passes
+    for (int i = warp; i < R; i += kCWarps)
+      for (int j = lane; j < n; j += 32) reinterpret_cast<T*>(P.Y)[(long)(r0 + i) * P.ld + j] = (T)(1.0 / dn);
+    if (c == 0 && tid == 0) {
+      *P.passes_out = 0;
+      P.sdsn_out[0] = 0.0; P.sdsn_out[1] = 0.0; P.sdsn_out[2] = 0.0;
+    }
+    cluster_sync();
+    return;
+  }
+  const double sc = (P.theta / 2.0) / m;                 // R11
+  if (c == 0 && tid == 0) P.sdsn_out[1] = m;
+
+  // the DSMEM slot of each of my columns in its owner's s_recv (owner k: k·n/C ≤ j < (k+1)·n/C),
+  // computed once (64-bit integer divisions are slow)
+  uint32_t dst_addr[kCColsPerThread];
+#pragma unroll
+  for (int u = 0; u < kCColsPerThread; ++u) {
+    const int j = tid + u * kCThreads;
+    dst_addr[u] = 0;
+    if (j < n) {
+      int kk = (int)min((long)(C - 1), (long)j * C / n);
+      while (kk > 0 && (long)kk * n / C > j) --kk;
+      while (kk + 1 < C && (long)(kk + 1) * n / C <= j) ++kk;
+      dst_addr[u] = dsmem(&s_recv[c * SL + (j - (int)((long)kk * n / C))], (unsigned)kk);
+    }
+  }
+  uint32_t sp_addr = 0;                                  // my mass slot in CTA `lane`'s s_Sp
+  if (warp == 0 && lane < C) sp_addr = dsmem(&s_Sp[c], (unsigned)lane);
+  double S = 0.0;                                       // mass of the current iterate (all CTAs)
+  // ---- one sweep over my rows, then the cluster all-reduce of column sums and mass ----
+  // mode 0: y ← fl(s·y) (or y when !scale); mode 1: y ← max(0, (y + a_i) + b_j)
+  auto sweep_and_reduce = [&](int mode) {
+    T colacc[kCMaxCols];
+#pragma unroll
+    for (int m2 = 0; m2 < kCMaxCols; ++m2) colacc[m2] = (T)0;
+    for (int i = warp; i < R; i += kCWarps) {
+      const T a = mode ? s_a[i] : (T)0;
+      T rs = (T)0;
+#pragma unroll
+      for (int m2 = 0; m2 < kCMaxCols; ++m2) {
+        const int j = lane + 32 * m2;
+        if (j < n) {
+          const T x = Ys[i * ldn + j];
+          T y;
+          if (mode) {
+            y = (x + a) + s_b[j];                        // P1 then P2 (R9 grouping)
+            y = y > (T)0 ? y : (T)0;
+          } else {
+            y = P.scale ? (T)(sc * (double)x) : x;
+          }
+          Ys[i * ldn + j] = y;
+          rs += y;
+          colacc[m2] += y;
+        }
+      }
+      double r;
+      if constexpr (sizeof(T) == 8) r = warp_sum_d((double)rs);
+      else r = (double)warp_sum_f((float)rs);
+      if (lane == 0) {
+        s_r[i] = r;
+        s_rn[i] = div_n(r, dn, rn);
+      }
+    }
+#pragma unroll
+    for (int m2 = 0; m2 < kCMaxCols; ++m2) {
+      const int j = lane + 32 * m2;
+      if (j < n) s_cp[warp * ldn + j] = colacc[m2];
+    }
+    __syncthreads();
+    // CTA partial of column j (8 warps in order) → the owner CTA of j (DSMEM); my mass → every CTA
+#pragma unroll
+    for (int u = 0; u < kCColsPerThread; ++u) {
+      const int j = tid + u * kCThreads;
+      if (j < n) {
+        T p = s_cp[j];
+        for (int w = 1; w < kCWarps; ++w) p += s_cp[w * ldn + j];
+        dst_t<T>(dst_addr[u], p);
+      }
+    }
+    if (warp == 0) {
+      double s = 0.0;
+      for (int i = lane; i < R; i += 32) s += s_r[i];
+      s = warp_sum_d(s);
+      if (lane < C) dst_f64(sp_addr, s);
+    }
+    cluster_sync();
+    S = 0.0;                                             // every CTA: the masses in CTA order
+    for (int k = 0; k < C; ++k) S += s_Sp[k];
+    // my column slice: c_j = Σ over CTAs in order (FP64); b_j = −c_j/n → every CTA (DSMEM)
+    for (int j = k0 + tid; j < k1; j += kCThreads) {
+      double cs = 0.0;
+      for (int k = 0; k < C; ++k) cs += (double)s_recv[k * SL + (j - k0)];
+      const T bj = (T)(-div_n(cs, dn, rn));
+      for (int k = 0; k < C; ++k) dst_t<T>(dsmem(&s_b[j], (unsigned)k), bj);
+    }
+    cluster_sync();
+  };
+
+  sweep_and_reduce(0);
+  int jp = 0;
+  double gam = 0.0;
+  for (;; ++jp) {
+    gam = div_n(S, dn, rn) - 1.0;                        // γ_j
+    if (c == 0 && tid == 0 && P.gamma_hist) P.gamma_hist[jp] = gam;
+    const bool last = P.sdsn_fixed > 0 ? (jp + 1 >= P.sdsn_fixed)
+                                       : ((jp >= 1 && gam <= P.gamma_th) || jp + 1 >= P.sdsn_max);
+    const double abase = rn + div_n(S, nn, rnn);         // 1/n + S/n²
+    for (int i = tid; i < R; i += kCThreads) s_a[i] = (T)(abase - s_rn[i]);
+    __syncthreads();
+    const double S_in = S;
+    sweep_and_reduce(1);                                 // the last pass's exchange is harmless
+    if (last) {
+      S = S_in;                                          // sdsn_out[2]: S of the last pass input
+      break;
+    }
+  }
+  // D → global
+  for (int i = warp; i < R; i += kCWarps)
+    for (int j = lane; j < n; j += 32) reinterpret_cast<T*>(P.Y)[(long)(r0 + i) * P.ld + j] = Ys[i * ldn + j];
+  if (c == 0 && tid == 0) {
+    *P.passes_out = jp + 1;
+    P.sdsn_out[0] = gam;
+    P.sdsn_out[2] = S;
+  }
+}
+
+int cluster_size_for(long n) { return (int)std::min<long>(kCMaxCluster, std::max<long>(1, (n + 31) / 32)); }
+
+size_t cluster_smem(long n, int C, size_t ts) {
+  const long ldn = (n + 3) & ~3L;
+  const long R = (n + C - 1) / C, SL = (n + C - 1) / C;
+  return ((size_t)R * ldn + (size_t)kCWarps * ldn + (size_t)kCMaxCluster * SL + (size_t)ldn) * ts;
+}
+
+}  // namespace
+
+bool sdsn_cluster_supported(long n, bool f64) {
+  if (n < 1 || (n + 31) / 32 > kCMaxCols) return false;
+  const int C = cluster_size_for(n);
+  if ((n + C - 1) / C > kCMaxRows) return false;
+  return cluster_smem(n, C, f64 ? 8 : 4) <= (size_t)(227 * 1024 - 4096);
+}
+
+cudaError_t launch_sdsn_cluster(const SdsnParams& p, bool f64, cudaStream_t st) {
+  if (!sdsn_cluster_supported(p.n, f64)) return cudaErrorInvalidValue;
+  const int C = cluster_size_for(p.n);
+  const int ldn = (int)((p.n + 3) & ~3L);
+  const size_t dsm = cluster_smem(p.n, C, f64 ? 8 : 4);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(C);
+  cfg.blockDim = dim3(kCThreads);
+  cfg.dynamicSmemBytes = dsm;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaError_t e;
+  if (f64) {
+    auto fn = sdsn_cluster_kernel<double>;
+    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)) != cudaSuccess) return e;
+    if (C > 8 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+    return cudaLaunchKernelEx(&cfg, fn, p, ldn);
+  }
+  auto fn = sdsn_cluster_kernel<float>;
+  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)) != cudaSuccess) return e;
+  if (C > 8 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
+  return cudaLaunchKernelEx(&cfg, fn, p, ldn);
+}
+
+}  // namespace fram
