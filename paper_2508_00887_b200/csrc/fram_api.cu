@@ -235,7 +235,7 @@ fram_status gradient(fram_ctx* h, int op, bool haveK, cudaStream_t st) {
   return FRAM_OK;
 }
 
-// SDSN kernel choice: 4 = K4c (one cluster; FP64 n ≤ ~600, FP32 n ≤ 32), 2 = K4r (FP32 on chip,
+// SDSN kernel choice: 4 = K4c (one cluster; FP64 n ≤ ~600, FP32 n ≤ 160), 2 = K4r (FP32 on chip,
 // n ≤ 4096), 1 = K4 (streaming).  FRAM_SDSN_STREAM forces K4, FRAM_SDSN_NOCLUSTER skips K4c (dev
 // comparison of the kernels).
 int sdsn_kind(const fram_ctx* h, bool f64) {
@@ -243,8 +243,8 @@ int sdsn_kind(const fram_ctx* h, bool f64) {
   static const bool no_cluster = getenv("FRAM_SDSN_NOCLUSTER") != nullptr;
   if (force_stream) return 1;
   // K4c where it measured fastest (tools/sdsn_small_timing.py): FP64 up to its size limit (vs K4),
-  // FP32 only for n ≤ 32 (K4r is faster from n = 64 on)
-  if (!no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 32)) return 4;
+  // FP32 only for n ≤ 160 (K4r is faster from n ≈ 200 on)
+  if (!no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160)) return 4;
   if (!f64 && fram::sdsn_res_grid(h->n, h->num_sms) > 0) return 2;
   return 1;
 }

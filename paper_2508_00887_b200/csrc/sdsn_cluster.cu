@@ -17,6 +17,7 @@
 // stop decision are identical everywhere.
 #include <math_constants.h>
 #include <algorithm>
+#include <type_traits>
 #include "common.cuh"
 #include "internal.h"
 
@@ -44,7 +45,7 @@ template <typename T> __device__ __forceinline__ void dst_t(uint32_t a, T v);
 template <> __device__ __forceinline__ void dst_t<float>(uint32_t a, float v) { dst_f32(a, v); }
 template <> __device__ __forceinline__ void dst_t<double>(uint32_t a, double v) { dst_f64(a, v); }
 
-template <typename T>
+template <typename T, int MC>                              // MC ≥ ⌈n/32⌉ columns per lane
 __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P, int ldn) {
   extern __shared__ __align__(16) unsigned char dsm[];
   const int n = (int)P.n;
@@ -128,28 +129,43 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
   // ---- one sweep over my rows, then the cluster all-reduce of column sums and mass ----
   // mode 0: y ← fl(s·y) (or y when !scale); mode 1: y ← max(0, (y + a_i) + b_j)
   auto sweep_and_reduce = [&](int mode) {
-    T colacc[kCMaxCols];
+    T colacc[MC], bl[MC];
 #pragma unroll
-    for (int m2 = 0; m2 < kCMaxCols; ++m2) colacc[m2] = (T)0;
+    for (int m2 = 0; m2 < MC; ++m2) {
+      const int j = lane + 32 * m2;
+      colacc[m2] = (T)0;
+      bl[m2] = (mode && j < n) ? s_b[j] : (T)0;           // b of my columns, for every row
+    }
     for (int i = warp; i < R; i += kCWarps) {
       const T a = mode ? s_a[i] : (T)0;
       T rs = (T)0;
+      // loads, arithmetic and stores in separate unrolled loops (no branch between columns, so the
+      // columns' dependency chains overlap); columns ≥ n read and contribute 0
+      T xv[MC];
 #pragma unroll
-      for (int m2 = 0; m2 < kCMaxCols; ++m2) {
+      for (int m2 = 0; m2 < MC; ++m2) {
         const int j = lane + 32 * m2;
-        if (j < n) {
-          const T x = Ys[i * ldn + j];
-          T y;
-          if (mode) {
-            y = (x + a) + s_b[j];                        // P1 then P2 (R9 grouping)
-            y = y > (T)0 ? y : (T)0;
-          } else {
-            y = P.scale ? (T)(sc * (double)x) : x;
-          }
-          Ys[i * ldn + j] = y;
-          rs += y;
-          colacc[m2] += y;
+        xv[m2] = j < n ? Ys[i * ldn + j] : (T)0;
+      }
+#pragma unroll
+      for (int m2 = 0; m2 < MC; ++m2) {
+        const int j = lane + 32 * m2;
+        T y;
+        if (mode) {
+          y = (xv[m2] + a) + bl[m2];                     // P1 then P2 (R9 grouping)
+          y = y > (T)0 ? y : (T)0;
+        } else {
+          y = P.scale ? (T)(sc * (double)xv[m2]) : xv[m2];
         }
+        y = j < n ? y : (T)0;
+        xv[m2] = y;
+        rs += y;
+        colacc[m2] += y;
+      }
+#pragma unroll
+      for (int m2 = 0; m2 < MC; ++m2) {
+        const int j = lane + 32 * m2;
+        if (j < n) Ys[i * ldn + j] = xv[m2];
       }
       double r;
       if constexpr (sizeof(T) == 8) r = warp_sum_d((double)rs);
@@ -160,7 +176,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
       }
     }
 #pragma unroll
-    for (int m2 = 0; m2 < kCMaxCols; ++m2) {
+    for (int m2 = 0; m2 < MC; ++m2) {
       const int j = lane + 32 * m2;
       if (j < n) s_cp[warp * ldn + j] = colacc[m2];
     }
@@ -256,17 +272,24 @@ cudaError_t launch_sdsn_cluster(const SdsnParams& p, bool f64, cudaStream_t st) 
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  cudaError_t e;
-  if (f64) {
-    auto fn = sdsn_cluster_kernel<double>;
-    if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)) != cudaSuccess) return e;
+  const int mc = (int)((p.n + 31) / 32);
+  auto go = [&](auto tag, auto mc_c) -> cudaError_t {
+    using T = decltype(tag);
+    auto fn = sdsn_cluster_kernel<T, decltype(mc_c)::value>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+    if (e != cudaSuccess) return e;
     if (C > 8 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
     return cudaLaunchKernelEx(&cfg, fn, p, ldn);
-  }
-  auto fn = sdsn_cluster_kernel<float>;
-  if ((e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm)) != cudaSuccess) return e;
-  if (C > 8 && (e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1)) != cudaSuccess) return e;
-  return cudaLaunchKernelEx(&cfg, fn, p, ldn);
+  };
+  auto pick = [&](auto tag) -> cudaError_t {
+    if (mc <= 1) return go(tag, std::integral_constant<int, 1>{});
+    if (mc <= 2) return go(tag, std::integral_constant<int, 2>{});
+    if (mc <= 4) return go(tag, std::integral_constant<int, 4>{});
+    if (mc <= 8) return go(tag, std::integral_constant<int, 8>{});
+    if (mc <= 16) return go(tag, std::integral_constant<int, 16>{});
+    return go(tag, std::integral_constant<int, kCMaxCols>{});
+  };
+  return f64 ? pick(double{}) : pick(float{});
 }
 
 }  // namespace fram
