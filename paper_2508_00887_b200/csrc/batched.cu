@@ -173,6 +173,13 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
   const int n = P.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long nn = (long)n * n;
   const double dn = (double)n;
+  // x/n and x/n² as RN(x/d) from a precomputed correctly rounded reciprocal plus one FMA correction
+  // (Markstein; exactly the IEEE quotient, see tools/div_probe.cu) — no FP64 division per pass
+  const double rdn = __drcp_rn(dn), rdnn = __drcp_rn(dn * dn);
+  auto div_n = [&](double x, double d, double r) {
+    const double q = x * r;
+    return fma(r, fma(-q, d, x), q);
+  };
   for (size_t i = tid * 16; i < off; i += BT * 16) *reinterpret_cast<uint4*>(sm + i) = make_uint4(0, 0, 0, 0);
   if (tid < 3) s_bad[tid] = 0;
   __syncthreads();
@@ -298,28 +305,47 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
       __syncthreads();
       for (int j = 0;; ++j) {
         const double S = s_scal[2];
-        const double gam = S / dn - 1.0;
+        const double gam = div_n(S, dn, rdn) - 1.0;
         const bool last = fixed > 0 ? (j + 1 >= fixed) : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
-        if (tid < NP) sa[tid] = (T)((1.0 / dn + S / (dn * dn)) - sr[tid] / dn);
-        else if (tid < 2 * NP) sb[tid - NP] = (T)(-sc[tid - NP] / dn);
+        if (tid < NP) sa[tid] = (T)((rdn + div_n(S, dn * dn, rdnn)) - div_n(sr[tid], dn, rdn));
+        else if (tid < 2 * NP) sb[tid - NP] = (T)(-div_n(sc[tid - NP], dn, rdn));
         __syncthreads();
         T cp0 = (T)0, cp1 = (T)0;
         const T b0 = sb[lane], b1 = sb[lane + 32];
-        for (int i = warp; i < n; i += BW) {
-          const T a = sa[i];
+        // the warp's (≤ NP/BW = 8) rows: per-lane row partials kept in registers and reduced together
+        // by one transpose-reduce (xor 16, 8, 4 halve the rows a lane carries, xor 2, 1 finish)
+        T rv[NP / BW];
+#pragma unroll
+        for (int k = 0; k < NP / BW; ++k) {
+          const int i = warp + k * BW;
           T y0 = (T)0, y1 = (T)0;
-          if (lane < n) { y0 = (sY[i * LDY + lane] + a) + b0; y0 = y0 > (T)0 ? y0 : (T)0; sY[i * LDY + lane] = y0; }
-          if (lane + 32 < n) {
-            y1 = (sY[i * LDY + lane + 32] + a) + b1;
-            y1 = y1 > (T)0 ? y1 : (T)0;
-            sY[i * LDY + lane + 32] = y1;
+          if (i < n) {
+            const T a = sa[i];
+            if (lane < n) { y0 = (sY[i * LDY + lane] + a) + b0; y0 = y0 > (T)0 ? y0 : (T)0; sY[i * LDY + lane] = y0; }
+            if (lane + 32 < n) {
+              y1 = (sY[i * LDY + lane + 32] + a) + b1;
+              y1 = y1 > (T)0 ? y1 : (T)0;
+              sY[i * LDY + lane + 32] = y1;
+            }
           }
           cp0 += y0;
           cp1 += y1;
-          T rs = y0 + y1;
+          rv[k] = y0 + y1;
+        }
+        {
+          static_assert(NP / BW == 8, "transpose-reduce of 8 rows");
+          const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+          T w4[4];
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) rs += __shfl_xor_sync(0xffffffffu, rs, o);
-          if (lane == 0) sr[i] = (double)rs;
+          for (int q = 0; q < 4; ++q) w4[q] = (b4 ? rv[q + 4] : rv[q]) + __shfl_xor_sync(0xffffffffu, b4 ? rv[q] : rv[q + 4], 16);
+          T w2[2];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) w2[q] = (b3 ? w4[q + 2] : w4[q]) + __shfl_xor_sync(0xffffffffu, b3 ? w4[q] : w4[q + 2], 8);
+          T z = (b2 ? w2[1] : w2[0]) + __shfl_xor_sync(0xffffffffu, b2 ? w2[0] : w2[1], 4);
+          z += __shfl_xor_sync(0xffffffffu, z, 2);
+          z += __shfl_xor_sync(0xffffffffu, z, 1);
+          const int i = warp + (lane >> 2) * BW;           // lane 4k holds row k of this warp
+          if ((lane & 3) == 0 && i < n) sr[i] = (double)z;
         }
         cpart[warp * NP + lane] = cp0;
         cpart[warp * NP + lane + 32] = cp1;
