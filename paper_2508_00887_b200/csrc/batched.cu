@@ -157,7 +157,6 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
   T* sK = reinterpret_cast<T*>(carve(sizeof(T) * NP * LDY));
   T* sY = reinterpret_cast<T*>(carve(sizeof(T) * NP * LDY));
   double* sr = reinterpret_cast<double*>(carve(sizeof(double) * NP));
-  double* sc = reinterpret_cast<double*>(carve(sizeof(double) * NP));
   T* sa = reinterpret_cast<T*>(carve(sizeof(T) * NP));
   T* sb = reinterpret_cast<T*>(carve(sizeof(T) * NP));
   T* cpart = reinterpret_cast<T*>(carve(sizeof(T) * BW * NP));
@@ -281,16 +280,21 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
         cpart[warp * NP + lane] = cp0;
         cpart[warp * NP + lane + 32] = cp1;
       };
-      auto finish = [&]() {   // c_j (fixed order over warps) and S (fixed order) after a sync
+      // after a sync: c_j (fixed order over warps) → b_j, and (warp 2) S (fixed order) → a_i for the
+      // next pass, so a pass needs one barrier after its sweep and one after this step
+      auto finish = [&]() {
         if (tid < NP) {
           double cs = 0.0;
 #pragma unroll
           for (int w = 0; w < BW; ++w) cs += (double)cpart[w * NP + tid];
-          sc[tid] = cs;
+          sb[tid] = (T)(-div_n(cs, dn, rdn));
         } else if (warp == 2) {
           double S = (lane < n ? sr[lane] : 0.0) + (lane + 32 < n ? sr[lane + 32] : 0.0);
           S = warp_sum_d(S);
           if (lane == 0) s_scal[2] = S;
+          const double ab = rdn + div_n(S, dn * dn, rdnn);
+          sa[lane] = (T)(ab - div_n(sr[lane], dn, rdn));
+          sa[lane + 32] = (T)(ab - div_n(sr[lane + 32], dn, rdn));
         }
       };
       if (scale)
@@ -307,9 +311,6 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
         const double S = s_scal[2];
         const double gam = div_n(S, dn, rdn) - 1.0;
         const bool last = fixed > 0 ? (j + 1 >= fixed) : ((j >= 1 && gam <= P.gamma_th) || j + 1 >= P.sdsn_max);
-        if (tid < NP) sa[tid] = (T)((rdn + div_n(S, dn * dn, rdnn)) - div_n(sr[tid], dn, rdn));
-        else if (tid < 2 * NP) sb[tid - NP] = (T)(-div_n(sc[tid - NP], dn, rdn));
-        __syncthreads();
         T cp0 = (T)0, cp1 = (T)0;
         const T b0 = sb[lane], b1 = sb[lane + 32];
         // the warp's (≤ NP/BW = 8) rows: per-lane row partials kept in registers and reduced together
@@ -457,7 +458,7 @@ size_t smem_bytes() {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   size_t s = 3 * r(sizeof(OT) * NP * LDO);
   if (OP != 0) s += r(sizeof(OT) * NP * LDO);
-  s += r(sizeof(double) * NP * LDO) + 2 * r(sizeof(T) * NP * LDY) + 2 * r(sizeof(double) * NP) +
+  s += r(sizeof(double) * NP * LDO) + 2 * r(sizeof(T) * NP * LDY) + r(sizeof(double) * NP) +
        2 * r(sizeof(T) * NP) + r(sizeof(T) * BW * NP) + r(sizeof(double) * BW * 4) + r(sizeof(double) * (NP + 1) * 3) +
        r(sizeof(int) * (NP + 1) * 2) + r(NP + 1);
   return s;
