@@ -61,6 +61,7 @@ struct fram_ctx {
   // workspace
   DevBuf Aq, BqT, Kq, N, Nq, UT, Y, colpart, Spart, Mpart, cvec, bar, scal, ghist, upd, lapw, permd;
   DevBuf rcolpart, rbvec, rflags, rdbg;
+  bool no_cluster = false;   // K4c could not be launched here once: use K4/K4r from then on
   DevBuf shUT, shUblk, shRsum, shSend, shRecv, shState, shNfull, shColpart, shScan;   // sharded solve
   DevBuf atA, atB, atK, atF, atFt, atPerm;                                           // attributed solve   // on-chip-resident SDSN (K4r)
   DevBuf stA, stB, stK, stX0, stX;
@@ -244,7 +245,7 @@ int sdsn_kind(const fram_ctx* h, bool f64) {
   if (force_stream) return 1;
   // K4c where it measured fastest (tools/sdsn_small_timing.py): FP64 up to its size limit (vs K4),
   // FP32 only for n ≤ 160 (K4r is faster from n ≈ 200 on)
-  if (!no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160)) return 4;
+  if (!no_cluster && !h->no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160)) return 4;
   if (!f64 && fram::sdsn_res_grid(h->n, h->num_sms) > 0) return 2;
   return 1;
 }
@@ -265,9 +266,18 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
     p.passes_out = reinterpret_cast<int*>(scal + 8);
     p.gamma_hist = h->ghist.as<double>();
     p.sdsn_out = scal;
-    CK(fram::launch_sdsn_cluster(p, f64, st), "sdsn (cluster) launch");
-    h->launches += 1;
-    return FRAM_OK;
+    const cudaError_t ce = fram::launch_sdsn_cluster(p, f64, st);
+    if (ce == cudaSuccess) {
+      h->launches += 1;
+      return FRAM_OK;
+    }
+    // a 16-CTA cluster may not be schedulable (e.g. on a partitioned GPU): clear the launch error and
+    // take the kernel the size would use without K4c
+    if (ce != cudaErrorInvalidClusterSize && ce != cudaErrorLaunchOutOfResources && ce != cudaErrorInvalidValue &&
+        ce != cudaErrorNotSupported)
+      CK(ce, "sdsn (cluster) launch");
+    cudaGetLastError();
+    h->no_cluster = true;
   }
   if (use_resident(h, f64)) {
     fram::ResParams r{};
