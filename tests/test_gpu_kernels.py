@@ -81,6 +81,22 @@ def test_gradient_mixed_multi_tile(prec, n):
     test_gradient_mixed(prec, n)
 
 
+@pytest.mark.parametrize("n,kind", [(2100, "random"), (3000, "nearperm"), (5000, "nearperm"), (6000, "twoperm")])
+def test_lap_cluster_sizes_bit_exact(n, kind):
+    # 2048 < n ≤ 8192 runs the R17 Hungarian on a 4-CTA cluster (K7c: columns split over the CTAs,
+    # records exchanged by st.async/mbarrier, u/p/way replicated): bit-exact with the oracle
+    rng = _rng(7000 + n)
+    if kind == "random":
+        N = rng.random((n, n))
+    elif kind == "nearperm":
+        N = 0.8 * random_perm_matrix(rng, n) + 0.2 * rng.random((n, n)) / n
+    else:
+        N = 0.5 * random_perm_matrix(rng, n) + 0.45 * random_perm_matrix(rng, n) + 0.05 * rng.random((n, n))
+    h = fram_create(n)
+    p = fram_lap(h, _g(N)).cpu().numpy()
+    assert np.array_equal(p, oracle.lap_max(N))
+
+
 def test_gradient_bf16_storage_input():
     # FRAM_DT_BF16 inputs (C5 stores A dense in BF16): same result as the FP64 copy of those values.
     n = 96
