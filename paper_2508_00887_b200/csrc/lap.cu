@@ -190,10 +190,10 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
 // trow[], known to all from the records, by the same FP64 adds in the same order) and pw[j] = way[j]
 // of the tree columns (final once a column is used, sent in its record).  way[] of the free columns
 // stays local (wl[]).  All float operations equal lap_kernel's, so the result is bit-exact with R17.
-template <int CS, int CPT>
-__global__ void __launch_bounds__(512, 1) lap_cluster_kernel(const double* __restrict__ N, int n, long ld,
-                                                             int32_t* perm) {
-  constexpr int THREADS = 512, WARPS = 16, CH = THREADS * CPT, NREC = CS * WARPS;
+template <int CS, int CPT, int THREADS = 512>
+__global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* __restrict__ N, int n, long ld,
+                                                                 int32_t* perm) {
+  constexpr int WARPS = THREADS / 32, CH = THREADS * CPT, NREC = CS * WARPS;
   constexpr uint32_t REC_BYTES = NREC * 16;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ __align__(16) uint4 s_rec[2][NREC];     // {key lo, key hi, j, way[j]} per warp per CTA
@@ -358,16 +358,16 @@ __global__ void __launch_bounds__(512, 1) lap_cluster_kernel(const double* __res
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int CS, int CPT>
+template <int CS, int CPT, int THREADS = 512>
 cudaError_t launch_cluster_t(const double* N, long n, long ld, int32_t* perm, cudaStream_t st) {
-  auto fn = lap_cluster_kernel<CS, CPT>;
+  auto fn = lap_cluster_kernel<CS, CPT, THREADS>;
   const size_t m = (size_t)n + 1;
-  const size_t bytes = m * (sizeof(double) + 3 * sizeof(int)) + (size_t)512 * CPT * sizeof(int) + 64;
+  const size_t bytes = m * (sizeof(double) + 3 * sizeof(int)) + (size_t)THREADS * CPT * sizeof(int) + 64;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS);
-  cfg.blockDim = dim3(512);
+  cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = bytes;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -403,10 +403,11 @@ cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* wo
   if (n <= 512) return launch_t<512, 1>(N, n, ld, perm, work, st);
   if (n <= 1024) return launch_t<512, 2>(N, n, ld, perm, work, st);
   if (n <= 2048) return launch_t<512, 4>(N, n, ld, perm, work, st);
-  // 2048 < n ≤ 8192: a 4-CTA cluster (C4, n = 4096: 96.5 ms against 120.0 ms on one CTA; 2 CTAs
-  // 100.5 ms, 8 CTAs 111.8 ms); the replicated u/p/way/tree arrays (20 B per row) must fit in shared memory
-  if (n <= 4096) return launch_cluster_t<4, 2>(N, n, ld, perm, st);
-  if (n <= 8192) return launch_cluster_t<4, 4>(N, n, ld, perm, st);
+  // 2048 < n ≤ 8192: a cluster of 4 CTAs × 256 threads (C4, n = 4096: 86.7 ms against 120.0 ms on
+  // one CTA; measured 2/4/8/16 CTAs × 128–1024 threads: 86.7–125 ms); the replicated u/p/way/tree arrays
+  // (20 B per row) must fit in shared memory
+  if (n <= 4096) return launch_cluster_t<4, 4, 256>(N, n, ld, perm, st);
+  if (n <= 8192) return launch_cluster_t<4, 8, 256>(N, n, ld, perm, st);
   if (n <= 16384) return launch_t<1024, 16>(N, n, ld, perm, work, st);
   if (n <= 65536) return launch_t<1024, 64>(N, n, ld, perm, work, st);
   return cudaErrorInvalidValue;
