@@ -12,5 +12,5 @@ timeout 600 $CMD > $OUT/plain_${TAG}.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file $OUT/launches_${TAG}.csv $CMD > $OUT/ncu_launch_${TAG}.log 2>&1; echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdsn -s 3 -c 1 -o $OUT/prof_sdsn_${TAG} $CMD > $OUT/ncu_sdsn_${TAG}.log 2>&1; echo "ncu sdsn rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 4 -c 2 -o $OUT/prof_gemm_${TAG} $CMD > $OUT/ncu_gemm_${TAG}.log 2>&1; echo "ncu gemm rc=$?"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:lap_kernel -c 1 -o $OUT/prof_lap_${TAG} $CMD > $OUT/ncu_lap_${TAG}.log 2>&1; echo "ncu lap rc=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:lap_ -c 1 -o $OUT/prof_lap_${TAG} $CMD > $OUT/ncu_lap_${TAG}.log 2>&1; echo "ncu lap rc=$?"
 ls -la $OUT
