@@ -131,3 +131,29 @@ def test_fram_c4_full_size_bf16():
     assert acc >= 0.95                                   # [M16]: 0.9795 on the CPU transcription
     # one outer iteration checked against the oracle on the same gradient input (sampled rows)
     assert stats["total_passes"] == sum(stats["passes"])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5])
+@pytest.mark.parametrize("prec", ["fp64", "bf16"])
+def test_fram_tiny_sizes(n, prec):
+    # degenerate sizes: one node (the only permutation), two and three nodes (ragged everywhere)
+    rng = np.random.Generator(np.random.PCG64(100 + n))
+    A = rng.random((n, n))
+    A = A + A.T
+    sig = rng.permutation(n)
+    B = np.empty_like(A)
+    B[np.ix_(sig, sig)] = A                             # B[σ(i), σ(j)] = A[i, j] (R18)
+    h = fram_create(n, schedule=Schedule(theta=10.0))
+    st, stats, X, perm = fram_solve(h, _g(A), _g(B), precision=prec)
+    assert st in (FRAM_OK, FRAM_NOT_CONVERGED)
+    p = perm.cpu().numpy()
+    assert sorted(p) == list(range(n))
+    Xn = X.cpu().numpy()
+    assert np.all(Xn >= 0)
+    assert np.array_equal(p, oracle.lap_max(Xn))
+    if prec == "fp64":
+        ref = oracle.fram(A, B, None, theta=10.0, replay=stats["passes"])
+        assert np.max(np.abs(Xn - ref["N"])) <= 1e-9
+        assert np.array_equal(p, ref["perm"])
+    if n == 1:
+        assert p[0] == 0 and abs(Xn[0, 0] - 1.0) <= 1e-6
