@@ -16,6 +16,11 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool pred
   const int sz = pred ? 16 : 0;
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
 }
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, bool pred) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  const int sz = pred ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void cp_wait0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
@@ -51,8 +56,18 @@ __global__ void __launch_bounds__(THREADS) gemm_f64_kernel(const double* __restr
       cp_async16(&As[buf][r][kc], ok ? (const void*)(A + gr * ld + gk) : (const void*)A, ok);
       const long gn = n0 + r;
       const bool okb = gn < N && gk < K;
-      const double* bp = kchunk ? B + (gk / kchunk) * N * kchunk + gn * kchunk + gk % kchunk : B + gn * ld + gk;
-      cp_async16(&Bs[buf][r][kc], okb ? (const void*)bp : (const void*)B, okb);
+      if (kchunk & 1) {                               // odd blocks: 8-byte copies (no 16-B alignment)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const long k = gk + e;
+          const bool oke = gn < N && k < K;
+          const double* bp = B + (k / kchunk) * N * kchunk + gn * kchunk + k % kchunk;
+          cp_async8(&Bs[buf][r][kc + e], oke ? (const void*)bp : (const void*)B, oke);
+        }
+      } else {
+        const double* bp = kchunk ? B + (gk / kchunk) * N * kchunk + gn * kchunk + gk % kchunk : B + gn * ld + gk;
+        cp_async16(&Bs[buf][r][kc], okb ? (const void*)bp : (const void*)B, okb);
+      }
     }
     cp_commit();
   };

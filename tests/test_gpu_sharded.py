@@ -50,6 +50,38 @@ def test_sharded_w1_fp64_c2_small_unary_replay():
     assert np.array_equal(perm.cpu().numpy(), oracle.lap_max(X.cpu().numpy()))
 
 
+def test_sharded_w1_fp64_several_rows_per_cta_replay():
+    # n = 437 on 148 CTAs: 2-3 rows per CTA, so the snake row order of odd passes and the per-CTA row
+    # offsets are exercised (n ≤ 148 gives every CTA one row)
+    inst = config_c2(2, n=437)
+    h = _sharded(inst.n, theta=inst.theta, flags=fb.FLAG_TRACE, max_outer=3)
+    st, stats, X, perm = fb.fram_solve(h, _g(inst.A), _g(inst.B), precision="fp64")
+    ref = oracle.fram(inst.A, inst.B, None, theta=inst.theta, max_outer=3, replay=stats["passes"])
+    assert np.max(np.abs(X.cpu().numpy() - ref["N"])) <= 1e-9
+    assert np.array_equal(perm.cpu().numpy(), oracle.lap_max(X.cpu().numpy()))
+
+
+def test_sharded_w1_fp64_long_rows_closed_form():
+    # n = 8200 in FP64: a row is 4100 two-element vectors, more than one 4096-vector work unit of
+    # K4s (the single-GPU path stops at n = 8192 in FP64).  With A = Ã = 0 the gradient is the
+    # constant λK' (K' = K/max K), so D = SDSN(λK') every iteration and closed form C
+    # gives N_t = D + (1−α)^t (N_0 − D); D comes from the oracle's Alg. 2 with the same 7 passes.
+    n, alpha = 8200, 0.95
+    rng = np.random.Generator(np.random.PCG64(11))
+    K = rng.random((n, n)) * 0.01
+    K[np.diag_indices(n)] += 1.0
+    Kp = K / K.max()
+    D, _ = oracle.sdsn(Kp, theta=10.0, sdsn_fixed=7)
+    N0 = np.full((n, n), 1.0 / n)
+    want = D + (1.0 - alpha) ** 2 * (N0 - D)
+    Z = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    h = _sharded(n, theta=10.0, alpha=alpha, sdsn_fixed=7, max_outer=2)
+    _, stats, X, perm = fb.fram_solve(h, Z, Z, _g(K), precision="fp64")
+    assert stats["passes"] == [7, 7]
+    assert np.max(np.abs(X.cpu().numpy() - want)) <= 1e-9
+    assert np.array_equal(perm.cpu().numpy(), np.arange(n))
+
+
 @pytest.mark.parametrize("prec", ["bf16", "tf32"])
 def test_sharded_w1_mixed_matches_single_gpu(prec):
     inst = config_c2(1, n=256)
