@@ -95,8 +95,12 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
   constexpr int WPR = VPL * (int)sizeof(VT) / 4;             // 32-bit words per thread per row
   extern __shared__ __align__(16) unsigned char dsm[];
   const long rows_max = (P.n + gridDim.x - 1) / gridDim.x + 1;
+  // b of the thread's column slots in shared memory for VPL ≥ 4 ([VPL][threads], conflict-free):
+  // in registers they pushed the sweep into spills (VPL = 8: 32 FP32 / 64 FP64 registers)
+  constexpr bool BSM = VPL >= 4;
   double* s_rowpart = reinterpret_cast<double*>(dsm);       // [rows_max][CG]
-  T* s_colstage = reinterpret_cast<T*>(dsm + ((sizeof(double) * rows_max * CG + 15) & ~15ul));   // [RG][ld]
+  VT* s_bv = reinterpret_cast<VT*>(dsm + ((sizeof(double) * rows_max * CG + 15) & ~15ul));   // [VPL][threads] (BSM)
+  T* s_colstage = reinterpret_cast<T*>(reinterpret_cast<unsigned char*>(s_bv) + (BSM ? (size_t)VPL * kSdsnThreads * sizeof(VT) : 0));   // [RG][ld]
   // On-chip rows (RG = 1 only, NT + NSM > 0): a warp's first NT rows live in TMEM (lane quarter
   // warp%4, column block (row·4 + warp/4)·WPR), the next NSM rows in shared memory, the rest stream
   // through L2/HBM.  A pass then moves only the streamed rows through the memory system (FP64 at
@@ -210,12 +214,22 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     // per-slot constants (32-bit indexing: n·ld < 2^31 for every supported n)
     const int ldv = (int)(ld / W);
     VT* Yc = reinterpret_cast<VT*>(Y) + (long)r0 * ldv;        // this CTA's first row
-    int qv[VPL], kind[VPL];                                   // kind: 0 skip, 1 full vector, 2 tail
+    // slot k's vector index and kind (0 skip, 1 full vector, 2 ragged tail), derived on use rather
+    // than kept in 2·VPL registers
+    const int q0 = (int)qidx(0);
+    auto qvf = [&](int k) -> int { return q0 + 32 * k; };
+    auto kindf = [&](int k) -> int {
+      const int q = q0 + 32 * k;
+      return q >= (int)nvec ? 0 : ((q + 1) * W <= (int)n ? 1 : 2);
+    };
+    auto getb = [&](int k, T (&bb)[W]) {
+      if constexpr (BSM) {
+        if constexpr (decltype(mode_c)::value == SWEEP_PASS) vget<T>(s_bv[k * kSdsnThreads + tid], bb);
+      } else {
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) {
-      qv[k] = (int)qidx(k);
-      kind[k] = qv[k] >= (int)nvec ? 0 : ((qv[k] + 1) * W <= (int)n ? 1 : 2);
-    }
+        for (int w = 0; w < W; ++w) bb[w] = bv[k][w];
+      }
+    };
     VT buf[PD][VPL];
     // on-chip rows first (local rows [0, non)), then the streamed rows with the register ring.
     // rev: the streamed rows in reverse order (odd passes), so a pass starts on the rows the
@@ -227,11 +241,11 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       const VT* row = Yc + (rg + rmap(rr) * RG) * ldv;
 #pragma unroll
       for (int k = 0; k < VPL; ++k)
-        if (kind[k]) buf[s][k] = __ldcg(row + qv[k]);
+        if (kindf(k)) buf[s][k] = __ldcg(row + qvf(k));
     };
     bool full = true;                                          // every slot a full vector?
 #pragma unroll
-    for (int k = 0; k < VPL; ++k) full = full && (kind[k] == 1);
+    for (int k = 0; k < VPL; ++k) full = full && (kindf(k) == 1);
     full = __all_sync(0xffffffffu, full);
     // the first streamed rows' loads are in flight while the on-chip rows are processed
 #pragma unroll
@@ -246,35 +260,36 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       if (mode_c.value == SWEEP_SCALE) {
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
-          if (kind[k]) vec(k) = __ldcg(row + qv[k]);
+          if (kindf(k)) vec(k) = __ldcg(row + qvf(k));
       } else if (il < NT) {
         tmem_ld<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
         tmem_wait_ld();
       } else {
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
-          if (kind[k]) vec(k) = s_on[(long)(il - NT) * nvec + qv[k]];
+          if (kindf(k)) vec(k) = s_on[(long)(il - NT) * nvec + qvf(k)];
       }
       const T a = (mode_c.value == SWEEP_PASS) ? s_a[il] : (T)0;
       T r = (T)0;
 #pragma unroll
       for (int k = 0; k < VPL; ++k) {
-        if (kind[k]) {
-          T x[W];
+        if (kindf(k)) {
+          T x[W], bb[W];
           vget<T>(vec(k), x);
+          getb(k, bb);
 #pragma unroll
           for (int w = 0; w < W; ++w) {
             T y;
-            if constexpr (decltype(mode_c)::value == SWEEP_PASS) y = tmax0((x[w] + a) + bv[k][w]);
+            if constexpr (decltype(mode_c)::value == SWEEP_PASS) y = tmax0((x[w] + a) + bb[w]);
             else y = P.scale ? (T)(sc * (double)x[w]) : x[w];
-            if (kind[k] == 2 && qv[k] * W + w >= (int)n) y = (T)0;
+            if (kindf(k) == 2 && qvf(k) * W + w >= (int)n) y = (T)0;
             x[w] = y;
             r += y;
             colacc[k][w] += y;
           }
           vec(k) = vmake<T>(x);
-          if (il >= NT) s_on[(long)(il - NT) * nvec + qv[k]] = vec(k);
-          if (wb) __stcg(row + qv[k], vec(k));
+          if (il >= NT) s_on[(long)(il - NT) * nvec + qvf(k)] = vec(k);
+          if (wb) __stcg(row + qvf(k), vec(k));
         }
       }
       if (il < NT) tmem_st<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
@@ -295,20 +310,21 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
             const T a = (mode == SWEEP_PASS) ? s_a[il] : (T)0;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
-              if (FULL || kind[k]) {
-                T e[W];
+              if (FULL || kindf(k)) {
+                T e[W], bb[W];
                 vget<T>(buf[s][k], e);
+                getb(k, bb);
 #pragma unroll
                 for (int w = 0; w < W; ++w) {
                   T y;
-                  if constexpr (mode == SWEEP_PASS) y = tmax0((e[w] + a) + bv[k][w]);   // P2(P1(Y))
+                  if constexpr (mode == SWEEP_PASS) y = tmax0((e[w] + a) + bb[w]);   // P2(P1(Y))
                   else y = P.scale ? (T)(sc * (double)e[w]) : e[w];
-                  if (!FULL && kind[k] == 2 && qv[k] * W + w >= (int)n) y = (T)0;     // ragged tail
+                  if (!FULL && kindf(k) == 2 && qvf(k) * W + w >= (int)n) y = (T)0;     // ragged tail
                   e[w] = y;
                   rs[s] += y;
                   colacc[k][w] += y;
                 }
-                if (mode == SWEEP_PASS || P.scale) __stcg(row + qv[k], vmake<T>(e));
+                if (mode == SWEEP_PASS || P.scale) __stcg(row + qvf(k), vmake<T>(e));
               }
             }
             if (rr + PD < nrs) load_row(s, rr + PD);
@@ -466,10 +482,16 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
             if (!Tag<double>::ok(cw[k][w], ep)) { ok = false; cw[k][w] = Tag<double>::ld(P.cvec + qidx(k) * W + w); }
       } while (!ok);
 #pragma unroll
-      for (int k = 0; k < VPL; ++k)
+      for (int k = 0; k < VPL; ++k) {
+        T x[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w)
-          bv[k][w] = (qidx(k) * W + w < n) ? (T)(-div_n(Tag<double>::val(cw[k][w]), dn, rn)) : (T)0;
+        for (int w = 0; w < W; ++w) x[w] = (qidx(k) * W + w < n) ? (T)(-div_n(Tag<double>::val(cw[k][w]), dn, rn)) : (T)0;
+        if constexpr (BSM) s_bv[k * kSdsnThreads + tid] = vmake<T>(x);
+        else {
+#pragma unroll
+          for (int w = 0; w < W; ++w) bv[k][w] = x[w];
+        }
+      }
     }
     __syncthreads();                                  // s_scal[0] (S of epoch ep) from the reduction
     const double S = s_scal[0];
@@ -527,7 +549,8 @@ static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int 
   auto fn = sdsn_kernel<T, VPL>;
   const int RG = kSdsnWarps / cg;
   const long rows_max = (p.n + grid - 1) / grid + 1;
-  size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0);
+  size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0) +
+               (VPL >= 4 ? (size_t)VPL * kSdsnThreads * sizeof(typename VecT<T>::t) : 0);   // s_bv
   // on-chip rows (one row group only): up to 128/WPR rows in TMEM and as many rows as fit in the
   // shared memory that is left (227 KB opt-in minus the static arrays)
   int nt = 0, nsm = 0;
