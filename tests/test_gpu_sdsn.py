@@ -178,3 +178,17 @@ def test_sdsn_fp32_streaming_gamma_stop():
     assert abs(k - ko) <= max(2, 0.02 * ko)
     Dn = D.cpu().numpy().astype(np.float64)
     assert np.all(Dn >= 0.0)
+
+
+@pytest.mark.parametrize("n", [4100, 6007, 8192])
+def test_sdsn_fp64_streaming_sizes(n):
+    # FP64 above n = 4096: the streaming kernel with 8 vectors per lane (b and the column accumulators
+    # in shared memory), ragged row blocks and an odd column tail (6007); oracle at a fixed pass count.
+    X = random_nonneg(_rng(91 + n), n, "sparse")
+    k = 5
+    h = fram_create(n, schedule=Schedule(theta=10.0, sdsn_fixed=k))
+    D, kk, gam = fram_sdsn(h, _gpu(X, torch.float64), "fp64")
+    assert kk == k
+    Do, _, go = oracle.sdsn(X, 10.0, sdsn_fixed=k, return_gammas=True)
+    assert np.max(np.abs(D.cpu().numpy() - Do)) <= 1e-12
+    assert np.max(np.abs(np.array(gam[:k]) - np.array(go[:k]))) <= 1e-12
