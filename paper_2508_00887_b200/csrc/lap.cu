@@ -190,17 +190,20 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
 // trow[], known to all from the records, by the same FP64 adds in the same order) and pw[j] = way[j]
 // of the tree columns (final once a column is used, sent in its record).  way[] of the free columns
 // stays local (wl[]).  All float operations equal lap_kernel's, so the result is bit-exact with R17.
-template <int CS, int CPT, int THREADS = 512>
+template <int CS, int CPT, int THREADS, bool UG>
 __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* __restrict__ N, int n, long ld,
-                                                                 int32_t* perm) {
+                                                                 int32_t* perm, double* ug) {
   constexpr int WARPS = THREADS / 32, CH = THREADS * CPT, NREC = CS * WARPS;
   constexpr uint32_t REC_BYTES = NREC * 16;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ __align__(16) uint4 s_rec[2][NREC];     // {key lo, key hi, j, way[j]} per warp per CTA
   __shared__ __align__(8) uint64_t s_mb[2];          // records of step parity q complete
   const int m = n + 1;
-  double* u = reinterpret_cast<double*>(dsm);         // [m] replicated row potentials
-  int* p = reinterpret_cast<int*>(u + m);             // [m] replicated matching
+  // [m] replicated row potentials: in shared memory, or (UG, n > 8192, where 20 B per row no longer
+  // fit) in this CTA's private copy in global memory — u is read once per step (u[i0], issued with
+  // the row loads) and updated for the tree rows by the same thread every step
+  double* u = UG ? ug + (size_t)blockIdx.x * m : reinterpret_cast<double*>(dsm);
+  int* p = UG ? reinterpret_cast<int*>(dsm) : reinterpret_cast<int*>(u + m);   // [m] replicated matching
   int* pw = p + m;                                    // [m] way of tree columns (replicated)
   int* trow = pw + m;                                 // [m] rows that entered the tree (this search)
   int* wl = trow + m;                                 // [CH] way of this CTA's columns
@@ -358,12 +361,13 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-template <int CS, int CPT, int THREADS = 512>
-cudaError_t launch_cluster_t(const double* N, long n, long ld, int32_t* perm, cudaStream_t st) {
-  auto fn = lap_cluster_kernel<CS, CPT, THREADS>;
+template <int CS, int CPT, int THREADS = 512, bool UG = false>
+cudaError_t launch_cluster_t(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
+  auto fn = lap_cluster_kernel<CS, CPT, THREADS, UG>;
   const size_t m = (size_t)n + 1;
-  const size_t bytes = m * (sizeof(double) + 3 * sizeof(int)) + (size_t)THREADS * CPT * sizeof(int) + 64;
+  const size_t bytes = m * ((UG ? 0 : sizeof(double)) + 3 * sizeof(int)) + (size_t)THREADS * CPT * sizeof(int) + 64;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(CS);
@@ -377,7 +381,7 @@ cudaError_t launch_cluster_t(const double* N, long n, long ld, int32_t* perm, cu
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, N, (int)n, ld, perm);
+  return cudaLaunchKernelEx(&cfg, fn, N, (int)n, ld, perm, reinterpret_cast<double*>(work));
 }
 
 template <int THREADS, int CPT>
@@ -396,7 +400,13 @@ cudaError_t launch_t(const double* N, long n, long ld, int32_t* perm, void* work
 
 }  // namespace
 
-size_t lap_work_bytes(long n) { return (size_t)(n + 1) * (sizeof(double) + 2 * sizeof(int)) + 64; }
+// single-CTA kernel: u, p, way in global memory; cluster kernel with u in global memory (n > 8192):
+// one u copy per CTA of the cluster (≤ 16)
+size_t lap_work_bytes(long n) {
+  const size_t single = (size_t)(n + 1) * (sizeof(double) + 2 * sizeof(int)) + 64;
+  const size_t cl = n > 8192 ? (size_t)(n + 1) * sizeof(double) * 16 : 0;
+  return single > cl ? single : cl;
+}
 
 cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
   if (n <= 256) return launch_t<256, 1>(N, n, ld, perm, work, st);
@@ -406,8 +416,18 @@ cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* wo
   // 2048 < n ≤ 8192: a cluster of 4 CTAs × 256 threads (C4, n = 4096: 86.7 ms against 120.0 ms on
   // one CTA; measured 2/4/8/16 CTAs × 128–1024 threads: 86.7–125 ms); the replicated u/p/way/tree arrays
   // (20 B per row) must fit in shared memory
-  if (n <= 4096) return launch_cluster_t<4, 4, 256>(N, n, ld, perm, st);
-  if (n <= 8192) return launch_cluster_t<4, 8, 256>(N, n, ld, perm, st);
+  if (n <= 4096) return launch_cluster_t<4, 4, 256>(N, n, ld, perm, work, st);
+  if (n <= 8192) return launch_cluster_t<4, 8, 256>(N, n, ld, perm, work, st);
+#ifndef LAP_BIG
+#define LAP_BIG 1
+#endif
+#if LAP_BIG == 1
+  if (n <= 16384) return launch_cluster_t<8, 8, 256, true>(N, n, ld, perm, work, st);
+#elif LAP_BIG == 2
+  if (n <= 16384) return launch_cluster_t<4, 16, 256, true>(N, n, ld, perm, work, st);
+#elif LAP_BIG == 3
+  if (n <= 16384) return launch_cluster_t<16, 4, 256, true>(N, n, ld, perm, work, st);
+#endif
   if (n <= 16384) return launch_t<1024, 16>(N, n, ld, perm, work, st);
   if (n <= 65536) return launch_t<1024, 64>(N, n, ld, perm, work, st);
   return cudaErrorInvalidValue;

@@ -81,10 +81,12 @@ def test_gradient_mixed_multi_tile(prec, n):
     test_gradient_mixed(prec, n)
 
 
-@pytest.mark.parametrize("n,kind", [(2100, "random"), (3000, "nearperm"), (5000, "nearperm"), (6000, "twoperm")])
+@pytest.mark.parametrize("n,kind", [(2100, "random"), (3000, "nearperm"), (5000, "nearperm"), (6000, "twoperm"),
+                                    (9000, "twoperm"), (16384, "nearperm")])
 def test_lap_cluster_sizes_bit_exact(n, kind):
     # 2048 < n ≤ 8192 runs the R17 Hungarian on a 4-CTA cluster (K7c: columns split over the CTAs,
-    # records exchanged by st.async/mbarrier, u/p/way replicated): bit-exact with the oracle
+    # records exchanged by st.async/mbarrier, u/p/way replicated), 8192 < n ≤ 16384 on an 8-CTA
+    # cluster with each CTA's copy of u in global memory: bit-exact with the oracle
     rng = _rng(7000 + n)
     if kind == "random":
         N = rng.random((n, n))
