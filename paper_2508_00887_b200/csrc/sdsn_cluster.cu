@@ -1,8 +1,8 @@
 // sdsn_cluster.cu — K4c: SDSN (Alg. 2) for small n on ONE thread-block cluster
 // of C ≤ 16 CTAs (one per SM).  The whole iterate stays in the CTAs' shared memory, and the per-pass
-// all-reduce of the column sums and the mass goes through distributed shared memory (DSMEM) with
-// two cluster barriers, instead of the L2 round trips that dominate K4/K4r when a pass has only
-// 20–800 columns (C1, C2).
+// all-reduce of the column sums and the mass goes through distributed shared memory (DSMEM) —
+// st.async stores completing on the receivers' mbarriers, no cluster barrier per pass — instead of
+// the L2 round trips that dominate K4/K4r when a pass has only 20–800 columns (C1, C2).
 //
 // Same arithmetic as K4/K4r (readings R5, R9-R13): γ_j = S_j/n − 1 (lagged test),
 // a_i = (1/n + S/n²) − r_i/n and b_j = −c_j/n in FP64 rounded to T, y' = max(0, (y + a_i) + b_j); S/n,
@@ -41,6 +41,27 @@ __device__ __forceinline__ void dst_f32(uint32_t a, float v) {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+#ifndef K4C_MB
+#define K4C_MB 1
+#endif
+// st.async: a remote shared-memory store that completes its bytes on the receiver's mbarrier
+__device__ __forceinline__ void ast_b32(uint32_t a, uint32_t v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a), "r"(v), "r"(mb) : "memory");
+}
+__device__ __forceinline__ void ast_b64(uint32_t a, unsigned long long v, uint32_t mb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(a), "l"(v), "r"(mb) : "memory");
+}
+template <typename T> __device__ __forceinline__ void ast_t(uint32_t a, T v, uint32_t mb);
+template <> __device__ __forceinline__ void ast_t<float>(uint32_t a, float v, uint32_t mb) { ast_b32(a, __float_as_uint(v), mb); }
+template <> __device__ __forceinline__ void ast_t<double>(uint32_t a, double v, uint32_t mb) {
+  ast_b64(a, (unsigned long long)__double_as_longlong(v), mb);
+}
+__device__ __forceinline__ void mb_wait(uint32_t mb, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred pp; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 pp, [%1], %2; selp.u32 %0, 1, 0, pp; }"
+                 : "=r"(done) : "r"(mb), "r"(parity) : "memory");
+}
 template <typename T> __device__ __forceinline__ void dst_t(uint32_t a, T v);
 template <> __device__ __forceinline__ void dst_t<float>(uint32_t a, float v) { dst_f32(a, v); }
 template <> __device__ __forceinline__ void dst_t<double>(uint32_t a, double v) { dst_f64(a, v); }
@@ -63,11 +84,20 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
   T* s_cp = Ys + (size_t)Rmax * ldn;                     // [8][ldn] per-warp column partials
   T* s_recv = s_cp + (size_t)kCWarps * ldn;              // [C][SL] partials of my column slice
   T* s_b = s_recv + (size_t)kCMaxCluster * SL;           // [ldn] b_j, all columns
-  __shared__ double s_Sp[kCMaxCluster];                  // per-CTA masses (all-gathered)
+  __shared__ double s_Sp[2][kCMaxCluster];               // per-CTA masses (all-gathered), by call parity:
+                                                         // with the mbarrier hand-off a fast CTA's next
+                                                         // masses may land before a slow thread read these
   __shared__ double s_M[kCMaxCluster];                   // per-CTA maxima (all-gathered)
   __shared__ double s_r[kCMaxRows], s_rn[kCMaxRows];     // row sums and r_i/n of my rows
   __shared__ T s_a[kCMaxRows];
+  __shared__ __align__(8) uint64_t s_mb[2];              // [0]: my slice's partials + masses, [1]: all b
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&s_mb[0]);
+  if (K4C_MB && tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const double dn = (double)n, nn = dn * dn;
   const double rn = __drcp_rn(dn), rnn = __drcp_rn(nn);
   auto div_n = [&](double x, double d, double r) {
@@ -123,12 +153,37 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
       dst_addr[u] = dsmem(&s_recv[c * SL + (j - (int)((long)kk * n / C))], (unsigned)kk);
     }
   }
-  uint32_t sp_addr = 0;                                  // my mass slot in CTA `lane`'s s_Sp
-  if (warp == 0 && lane < C) sp_addr = dsmem(&s_Sp[c], (unsigned)lane);
+  uint32_t sp_addr = 0, sp_mb = 0;                       // my mass slot in CTA `lane`'s s_Sp (+ its mbarrier)
+  if (warp == 0 && lane < C) {
+    sp_addr = dsmem(&s_Sp[0][c], (unsigned)lane);
+    sp_mb = dsmem(&s_mb[0], (unsigned)lane);
+  }
+  // owner of each of my columns' mbarrier (partials), computed with the slots above
+  uint32_t dst_mb[kCColsPerThread];
+#pragma unroll
+  for (int u = 0; u < kCColsPerThread; ++u) {
+    const int j = tid + u * kCThreads;
+    dst_mb[u] = 0;
+    if (j < n) {
+      int kk = (int)min((long)(C - 1), (long)j * C / n);
+      while (kk > 0 && (long)kk * n / C > j) --kk;
+      while (kk + 1 < C && (long)(kk + 1) * n / C <= j) ++kk;
+      dst_mb[u] = dsmem(&s_mb[0], (unsigned)kk);
+    }
+  }
+  int call = 0;                                          // sweep_and_reduce calls: mbarrier phase parity
   double S = 0.0;                                       // mass of the current iterate (all CTAs)
   // ---- one sweep over my rows, then the cluster all-reduce of column sums and mass ----
   // mode 0: y ← fl(s·y) (or y when !scale); mode 1: y ← max(0, (y + a_i) + b_j)
   auto sweep_and_reduce = [&](int mode) {
+    const uint32_t par = (uint32_t)(call & 1);
+    ++call;
+    if (K4C_MB && tid == 0) {                            // bytes this pass brings: my slice from every
+      const uint32_t bp = (uint32_t)(C * ((k1 - k0) * (int)sizeof(T) + 8));   // CTA + C masses; all of b
+      const uint32_t bb = (uint32_t)(n * (int)sizeof(T));
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb0), "r"(bp) : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb0 + 8), "r"(bb) : "memory");
+    }
     T colacc[MC], bl[MC];
 #pragma unroll
     for (int m2 = 0; m2 < MC; ++m2) {
@@ -188,26 +243,35 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
       if (j < n) {
         T p = s_cp[j];
         for (int w = 1; w < kCWarps; ++w) p += s_cp[w * ldn + j];
-        dst_t<T>(dst_addr[u], p);
+        if (K4C_MB) ast_t<T>(dst_addr[u], p, dst_mb[u]);
+        else dst_t<T>(dst_addr[u], p);
       }
     }
     if (warp == 0) {
       double s = 0.0;
       for (int i = lane; i < R; i += 32) s += s_r[i];
       s = warp_sum_d(s);
-      if (lane < C) dst_f64(sp_addr, s);
+      if (lane < C) {
+        if (K4C_MB) ast_t<double>(sp_addr + par * (uint32_t)(kCMaxCluster * sizeof(double)), s, sp_mb);
+        else dst_f64(sp_addr, s);
+      }
     }
-    cluster_sync();
+    if (K4C_MB) mb_wait(mb0, par);                       // my slice's partials and every mass arrived
+    else cluster_sync();
     S = 0.0;                                             // every CTA: the masses in CTA order
-    for (int k = 0; k < C; ++k) S += s_Sp[k];
+    for (int k = 0; k < C; ++k) S += s_Sp[K4C_MB ? par : 0][k];
     // my column slice: c_j = Σ over CTAs in order (FP64); b_j = −c_j/n → every CTA (DSMEM)
     for (int j = k0 + tid; j < k1; j += kCThreads) {
       double cs = 0.0;
       for (int k = 0; k < C; ++k) cs += (double)s_recv[k * SL + (j - k0)];
       const T bj = (T)(-div_n(cs, dn, rn));
-      for (int k = 0; k < C; ++k) dst_t<T>(dsmem(&s_b[j], (unsigned)k), bj);
+      for (int k = 0; k < C; ++k) {
+        if (K4C_MB) ast_t<T>(dsmem(&s_b[j], (unsigned)k), bj, dsmem(&s_mb[1], (unsigned)k));
+        else dst_t<T>(dsmem(&s_b[j], (unsigned)k), bj);
+      }
     }
-    cluster_sync();
+    if (K4C_MB) mb_wait(mb0 + 8, par);                   // every b_j arrived
+    else cluster_sync();
   };
 
   sweep_and_reduce(0);
@@ -236,6 +300,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
     P.sdsn_out[0] = gam;
     P.sdsn_out[2] = S;
   }
+  if (K4C_MB) cluster_sync();
 }
 
 int cluster_size_for(long n) { return (int)std::min<long>(kCMaxCluster, std::max<long>(1, (n + 31) / 32)); }
