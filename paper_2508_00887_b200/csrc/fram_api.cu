@@ -244,7 +244,7 @@ int sdsn_kind(const fram_ctx* h, bool f64) {
   static const bool no_cluster = getenv("FRAM_SDSN_NOCLUSTER") != nullptr;
   if (force_stream) return 1;
   // K4c where it measured fastest (tools/sdsn_small_timing.py): FP64 up to its size limit (vs K4),
-  // FP32 only for n ≤ 160 (K4r is faster from n ≈ 200 on)
+  // FP32 only for n ≤ 160 (with the mbarrier hand-off K4c and K4r tie at n = 256, K4r is faster above)
   if (!no_cluster && !h->no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160)) return 4;
   if (!f64 && fram::sdsn_res_grid(h->n, h->num_sms) > 0) return 2;
   return 1;
