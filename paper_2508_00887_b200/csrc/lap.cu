@@ -418,17 +418,8 @@ cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* wo
   // (20 B per row) must fit in shared memory
   if (n <= 4096) return launch_cluster_t<4, 4, 256>(N, n, ld, perm, work, st);
   if (n <= 8192) return launch_cluster_t<4, 8, 256>(N, n, ld, perm, work, st);
-#ifndef LAP_BIG
-#define LAP_BIG 1
-#endif
-#if LAP_BIG == 1
+  // n ≤ 16384: 8 CTAs × 256 threads × 8 columns, u in global memory (4×16 and 16×4 measured slower)
   if (n <= 16384) return launch_cluster_t<8, 8, 256, true>(N, n, ld, perm, work, st);
-#elif LAP_BIG == 2
-  if (n <= 16384) return launch_cluster_t<4, 16, 256, true>(N, n, ld, perm, work, st);
-#elif LAP_BIG == 3
-  if (n <= 16384) return launch_cluster_t<16, 4, 256, true>(N, n, ld, perm, work, st);
-#endif
-  if (n <= 16384) return launch_t<1024, 16>(N, n, ld, perm, work, st);
   if (n <= 65536) return launch_t<1024, 64>(N, n, ld, perm, work, st);
   return cudaErrorInvalidValue;
 }

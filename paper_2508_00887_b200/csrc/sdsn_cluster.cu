@@ -35,15 +35,9 @@ __device__ __forceinline__ uint32_t dsmem(const void* p, unsigned rank) {
 __device__ __forceinline__ void dst_f64(uint32_t a, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
 }
-__device__ __forceinline__ void dst_f32(uint32_t a, float v) {
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-#ifndef K4C_MB
-#define K4C_MB 1
-#endif
 // st.async: a remote shared-memory store that completes its bytes on the receiver's mbarrier
 __device__ __forceinline__ void ast_b32(uint32_t a, uint32_t v, uint32_t mb) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a), "r"(v), "r"(mb) : "memory");
@@ -62,9 +56,6 @@ __device__ __forceinline__ void mb_wait(uint32_t mb, uint32_t parity) {
     asm volatile("{ .reg .pred pp; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 pp, [%1], %2; selp.u32 %0, 1, 0, pp; }"
                  : "=r"(done) : "r"(mb), "r"(parity) : "memory");
 }
-template <typename T> __device__ __forceinline__ void dst_t(uint32_t a, T v);
-template <> __device__ __forceinline__ void dst_t<float>(uint32_t a, float v) { dst_f32(a, v); }
-template <> __device__ __forceinline__ void dst_t<double>(uint32_t a, double v) { dst_f64(a, v); }
 
 template <typename T, int MC>                              // MC ≥ ⌈n/32⌉ columns per lane
 __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P, int ldn) {
@@ -93,7 +84,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
   __shared__ __align__(8) uint64_t s_mb[2];              // [0]: my slice's partials + masses, [1]: all b
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t mb0 = (uint32_t)__cvta_generic_to_shared(&s_mb[0]);
-  if (K4C_MB && tid == 0) {
+  if (tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb0 + 8));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -178,7 +169,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
   auto sweep_and_reduce = [&](int mode) {
     const uint32_t par = (uint32_t)(call & 1);
     ++call;
-    if (K4C_MB && tid == 0) {                            // bytes this pass brings: my slice from every
+    if (tid == 0) {                                      // bytes this pass brings: my slice from every
       const uint32_t bp = (uint32_t)(C * ((k1 - k0) * (int)sizeof(T) + 8));   // CTA + C masses; all of b
       const uint32_t bb = (uint32_t)(n * (int)sizeof(T));
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb0), "r"(bp) : "memory");
@@ -243,8 +234,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
       if (j < n) {
         T p = s_cp[j];
         for (int w = 1; w < kCWarps; ++w) p += s_cp[w * ldn + j];
-        if (K4C_MB) ast_t<T>(dst_addr[u], p, dst_mb[u]);
-        else dst_t<T>(dst_addr[u], p);
+        ast_t<T>(dst_addr[u], p, dst_mb[u]);
       }
     }
     if (warp == 0) {
@@ -252,26 +242,22 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
       for (int i = lane; i < R; i += 32) s += s_r[i];
       s = warp_sum_d(s);
       if (lane < C) {
-        if (K4C_MB) ast_t<double>(sp_addr + par * (uint32_t)(kCMaxCluster * sizeof(double)), s, sp_mb);
-        else dst_f64(sp_addr, s);
+        ast_t<double>(sp_addr + par * (uint32_t)(kCMaxCluster * sizeof(double)), s, sp_mb);
       }
     }
-    if (K4C_MB) mb_wait(mb0, par);                       // my slice's partials and every mass arrived
-    else cluster_sync();
+    mb_wait(mb0, par);                                   // my slice's partials and every mass arrived
     S = 0.0;                                             // every CTA: the masses in CTA order
-    for (int k = 0; k < C; ++k) S += s_Sp[K4C_MB ? par : 0][k];
+    for (int k = 0; k < C; ++k) S += s_Sp[par][k];
     // my column slice: c_j = Σ over CTAs in order (FP64); b_j = −c_j/n → every CTA (DSMEM)
     for (int j = k0 + tid; j < k1; j += kCThreads) {
       double cs = 0.0;
       for (int k = 0; k < C; ++k) cs += (double)s_recv[k * SL + (j - k0)];
       const T bj = (T)(-div_n(cs, dn, rn));
       for (int k = 0; k < C; ++k) {
-        if (K4C_MB) ast_t<T>(dsmem(&s_b[j], (unsigned)k), bj, dsmem(&s_mb[1], (unsigned)k));
-        else dst_t<T>(dsmem(&s_b[j], (unsigned)k), bj);
+        ast_t<T>(dsmem(&s_b[j], (unsigned)k), bj, dsmem(&s_mb[1], (unsigned)k));
       }
     }
-    if (K4C_MB) mb_wait(mb0 + 8, par);                   // every b_j arrived
-    else cluster_sync();
+    mb_wait(mb0 + 8, par);                               // every b_j arrived
   };
 
   sweep_and_reduce(0);
@@ -300,7 +286,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
     P.sdsn_out[0] = gam;
     P.sdsn_out[2] = S;
   }
-  if (K4C_MB) cluster_sync();
+  cluster_sync();                                        // no CTA exits while remote stores may target it
 }
 
 int cluster_size_for(long n) { return (int)std::min<long>(kCMaxCluster, std::max<long>(1, (n + 31) / 32)); }

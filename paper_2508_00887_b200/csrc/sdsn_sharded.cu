@@ -19,10 +19,7 @@
 namespace fram {
 namespace {
 
-#ifndef SH_THREADS
-#define SH_THREADS 512
-#endif
-constexpr int kShThreads = SH_THREADS;
+constexpr int kShThreads = 512;                  // 256 / 1024 measured slower (418 / 386 vs 375 us at C5)
 
 template <typename T> struct V4;
 template <> struct V4<float> { using t = float4; static constexpr int W = 4; };
