@@ -91,7 +91,10 @@ template <typename T, int VPL>
 __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int CG, int NT, int NSM) {
   using VT = typename VecT<T>::t;
   constexpr int W = VecT<T>::W;
-  constexpr int PD = VPL >= 8 ? 1 : 16 / VPL;                // rows in flight per warp
+  // rows in flight per warp: 2 for VPL = 2 and 4 (16/VPL measured slower — the deeper ring pushed
+  // the sweep into spills: FP64 n = 4096 32.4 → 27.4 us/pass, FP64 n = 2048 11.8 → 10.2, FP32
+  // n = 6000 44.4 → 35.6; PD = 3 / 4 for VPL = 4 / 2 in between)
+  constexpr int PD = VPL >= 8 ? 1 : VPL >= 2 ? 2 : 16;
   constexpr int WPR = VPL * (int)sizeof(VT) / 4;             // 32-bit words per thread per row
   extern __shared__ __align__(16) unsigned char dsm[];
   const long rows_max = (P.n + gridDim.x - 1) / gridDim.x + 1;
