@@ -98,9 +98,10 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
   constexpr int WPR = VPL * (int)sizeof(VT) / 4;             // 32-bit words per thread per row
   extern __shared__ __align__(16) unsigned char dsm[];
   const long rows_max = (P.n + gridDim.x - 1) / gridDim.x + 1;
-  // b of the thread's column slots in shared memory for VPL ≥ 4 ([VPL][threads], conflict-free):
-  // in registers they pushed the sweep into spills (VPL = 8: 32 FP32 / 64 FP64 registers)
-  constexpr bool BSM = VPL >= 4;
+  // b of the thread's column slots in shared memory for VPL = 8 ([VPL][threads], conflict-free):
+  // in registers they pushed the sweep into spills (32 FP32 / 64 FP64 registers); with the 2-row
+  // ring VPL = 4 keeps them in registers without spills (and one more on-chip row fits)
+  constexpr bool BSM = VPL >= 8;
   double* s_rowpart = reinterpret_cast<double*>(dsm);       // [rows_max][CG]
   VT* s_bv = reinterpret_cast<VT*>(dsm + ((sizeof(double) * rows_max * CG + 15) & ~15ul));   // [VPL][threads] (BSM)
   // column accumulators in shared memory as well for FP64 with VPL = 8 (CSM; one 16-byte read-modify-
@@ -593,7 +594,7 @@ static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int 
   const int RG = kSdsnWarps / cg;
   const long rows_max = (p.n + grid - 1) / grid + 1;
   size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0) +
-               (VPL >= 4 ? (size_t)VPL * kSdsnThreads * sizeof(typename VecT<T>::t) : 0) +  // s_bv
+               (VPL >= 8 ? (size_t)VPL * kSdsnThreads * sizeof(typename VecT<T>::t) : 0) +  // s_bv
                (VPL >= 8 && sizeof(T) == 8 ? (size_t)VPL * kSdsnThreads * sizeof(typename VecT<T>::t) : 0);   // s_cacc
   // on-chip rows (one row group only): up to 128/WPR rows in TMEM and as many rows as fit in the
   // shared memory that is left (227 KB opt-in minus the static arrays)
