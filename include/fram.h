@@ -186,7 +186,11 @@ FRAM_API fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, 
                           void* G_out, double* c_out);
 
 /* fram_lap: perm = argmax_π Σ_i N[i,π(i)] (Eq.(2); Alg.1 step 10) by the deterministic
- *   Hungarian of R17, bit-exact with the oracle's LAP given the same N (FP64). */
+ *   Hungarian of R17, bit-exact with the oracle's LAP given the same N (FP64).  N: host or device,
+ *   n×n contiguous row-major (copied into the handle's workspace); perm_out: host or device
+ *   int32[n]; returns after `stream` synchronizes.  One CTA for n ≤ 2048, a thread-block cluster
+ *   above (4 CTAs to 8192, 8 CTAs to 16384), one CTA again up to 65536; a larger n fails to launch
+ *   (FRAM_ERR_CUDA). */
 FRAM_API fram_status fram_lap(fram_handle h, const double* N, int32_t* perm_out, void* stream);
 
 /* Library/ABI version and the compile target ("sm_100a"). */
