@@ -150,7 +150,11 @@ def sdsn(X, theta, gamma_th=1e-3, sdsn_max=1000, sdsn_fixed=0, scale=True,
         gammas.append(g)
         a = (1.0 / n + S / (n * n)) - r / n
         b = -c / n
-        Y = np.maximum(0.0, (Y + a[:, None]) + b[None, :])
+        # Y = max(0, (Y + a) + b), evaluated in place (same operations in the same order,
+        # bit-identical to the out-of-place expression; Y is this function's own copy)
+        np.add(Y, a[:, None], out=Y)
+        np.add(Y, b[None, :], out=Y)
+        np.maximum(Y, 0.0, out=Y)
         j += 1
         if sdsn_fixed > 0:
             if j == sdsn_fixed:
@@ -171,7 +175,7 @@ def dsn_fixed(X, iters):
 # --------------------------------------------------------------------------------------
 def fram(A, B, K=None, lam=1.0, theta=10.0, alpha=0.95, gamma_th=1e-3, delta_th=1e-4,
          max_outer=100, sdsn_max=1000, sdsn_fixed=0, X0=None, replay=None, scale=True,
-         keep_trace=False):
+         keep_trace=False, on_iter=None):
     """FRAM — Algorithm 1, FP64 throughout.
 
     O1-O2 precondition (steps 2-3); O3 N⁽⁰⁾ = X0 or 11ᵀ/n (R1); do-while outer loop (R2):
@@ -181,6 +185,7 @@ def fram(A, B, K=None, lam=1.0, theta=10.0, alpha=0.95, gamma_th=1e-3, delta_th=
     Step 10: perm = LAP_max(N) (R17).
     `replay`: per-outer-iteration SDSN pass counts to replay (parity harness):
       exactly len(replay) outer iterations run, pass t uses replay[t-1] passes.
+    `on_iter(t, N, k_t, δ_t)`: optional observer called after each outer iteration.
     Returns a dict with N, perm, outer_iters, passes, deltas, converged, c and (keep_trace) Ns.
     """
     from .lap import lap_max
@@ -203,6 +208,8 @@ def fram(A, B, K=None, lam=1.0, theta=10.0, alpha=0.95, gamma_th=1e-3, delta_th=
         deltas.append(float(delta))
         if keep_trace:
             Ns.append(N.copy())
+        if on_iter is not None:          # observer only (checkpointing long runs); no arithmetic
+            on_iter(t, N, k, float(delta))
         if delta <= delta_th:
             converged = True
             if replay is None:
