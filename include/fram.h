@@ -83,7 +83,8 @@ typedef struct {
   int32_t sdsn_fixed;   /* 0 = γ test; >0 = exactly this many passes per call (DSPFP / parity)    */
   int32_t flags;        /* FRAM_FLAG_*                                                            */
   const int32_t* replay_passes;  /* host, nullable: pass count for outer iteration t (0-based);
-                                    when set, exactly replay_len outer iterations run           */
+                                    when set, exactly replay_len outer iterations run;
+                                    replay_len > max_outer → FRAM_ERR_USAGE                       */
   int32_t replay_len;
 } fram_schedule;
 
@@ -174,8 +175,8 @@ FRAM_API fram_status fram_create_sharded(int64_t n, double lambda, const fram_sc
 /* ---- test entry points (parity harness) ----------------------------------------------------
  * fram_sdsn: one SDSN call (Alg.2) on a nonnegative n×n X.  p = FRAM_PREC_FP64: X and
  *   D_out are FP64; any other p: FP32.  Uses the handle's θ, γ_th, sdsn_max, sdsn_fixed and the
- *   FRAM_FLAG_NO_THETA_SCALE flag.  passes: host int32 out.  gamma_hist: host double[sdsn_max]
- *   (nullable) receives γ_j of every pass input.  Negative X → FRAM_ERR_DATA. */
+ *   FRAM_FLAG_NO_THETA_SCALE flag.  passes: host int32 out.  gamma_hist: host
+ *   double[max(sdsn_max, sdsn_fixed)] (nullable) receives γ_j of every pass input.  Negative X → FRAM_ERR_DATA. */
 FRAM_API fram_status fram_sdsn(fram_handle h, fram_precision p, const void* X, void* D_out,
                       int32_t* passes, double* gamma_hist, void* stream);
 

@@ -25,6 +25,7 @@ from .fram_oracle import (  # noqa: F401
     p3_project,
     gamma,
     sdsn,
+    sdsn_fp32,
     dsn_fixed,
     fram,
     objective,

@@ -17,6 +17,12 @@ Pins (tests/test_oracle_*.py, all `-m "not gpu"`):
                   limits, scale invariance, permutation equivariance.
   fram          — closed form C (A=Ã=0), scale invariance, exact recovery on
                   noise-free isomorphic pairs, brute-force QAP at n<=8.
+  sdsn_fp32     — closed form B bit-exact in FP32 (n = 2^k), the uniform-input closed form
+                  (11ᵀ/n in 2 passes), FP32 storage, deviation from `sdsn` within the FP32
+                  rounding bound (tests/test_oracle_sdsn.py).
+  dsn_fixed     — one round = P2(P1(X)) on a non-uniform X (no θ-scaling).
+  matching_error— hand-computed 3-node example with and without the feature term.
+  objective_perm, node_accuracy — tests/test_oracle_fram.py (brute force, planted recovery).
 """
 from __future__ import annotations
 
@@ -162,6 +168,53 @@ def sdsn(X, theta, gamma_th=1e-3, sdsn_max=1000, sdsn_fixed=0, scale=True,
         elif (j - 1 >= 1 and g <= gamma_th) or j == sdsn_max:
             break
     return (Y, j, gammas) if return_gammas else (Y, j)
+
+
+def sdsn_fp32(X, theta, gamma_th=1e-3, sdsn_max=1000, sdsn_fixed=0, scale=True, return_gammas=False):
+    """SDSN (Alg. 2) with the iterate STORED IN FP32 — the emulated-rounding diagnostic
+    reference of SURVEY §8(c) ("Rounding helpers"), for the paper's FP32 step 6.
+
+    Same steps and grouping as `sdsn`; only the storage precision of Y differs (R9, R11, R13):
+      Y⁰ = fl32(s·X), s = (θ/2)/max X in FP64                         (step 1, R11)
+      r, c, S: FP64 sums of the FP32 values                            (R13)
+      a_i = fl32((1/n + S/n²) − r_i/n),  b_j = fl32(−c_j/n)            (FP64, rounded once, R9)
+      Y ← max(0, fl32(fl32(Y + a_i) + b_j))                            (step 6, FP32 adds)
+    γ_j = S_j/n − 1 in FP64; stopping rule as `sdsn` (R5).  Input X: values representable in FP32.
+    Returns (D as float64 holding FP32 values, passes[, gammas]).
+    """
+    X = _check_square(X)
+    n = X.shape[0]
+    if scale:
+        m = X.max()
+        if m == 0.0:
+            D = np.full((n, n), np.float32(1.0 / n), dtype=np.float64)
+            return (D, 0, []) if return_gammas else (D, 0)
+        s = (theta / 2.0) / m
+        Y = (s * X).astype(np.float32)
+    else:
+        Y = X.astype(np.float32)
+    gammas = []
+    j = 0
+    while True:
+        Y64 = Y.astype(np.float64)
+        r = Y64.sum(axis=1)
+        c = Y64.sum(axis=0)
+        S = r.sum()
+        g = S / n - 1.0
+        gammas.append(g)
+        a = ((1.0 / n + S / (n * n)) - r / n).astype(np.float32)
+        b = (-c / n).astype(np.float32)
+        np.add(Y, a[:, None], out=Y)                    # float32 + float32 → float32 (RNE)
+        np.add(Y, b[None, :], out=Y)
+        np.maximum(Y, np.float32(0.0), out=Y)
+        j += 1
+        if sdsn_fixed > 0:
+            if j == sdsn_fixed:
+                break
+        elif (j - 1 >= 1 and g <= gamma_th) or j == sdsn_max:
+            break
+    D = Y.astype(np.float64)
+    return (D, j, gammas) if return_gammas else (D, j)
 
 
 def dsn_fixed(X, iters):

@@ -38,7 +38,11 @@ struct DevBuf {
     cudaError_t e = cudaMalloc(&p, b);
     if (e != cudaSuccess) { p = nullptr; return e; }
     bytes = b;
-    return cudaMemset(p, 0, b);
+    // zero-filled before any caller stream (possibly non-blocking) can touch it: some kernels rely on
+    // the zero (the update kernel's arrival counter, ld padding columns of the operand buffers)
+    e = cudaMemset(p, 0, b);
+    if (e != cudaSuccess) return e;
+    return cudaDeviceSynchronize();
   }
   void release() { if (p) cudaFree(p); p = nullptr; bytes = 0; }
   template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
@@ -98,6 +102,8 @@ fram_status check_schedule(const fram_schedule& s) {
   if (!(s.delta_th >= 0)) return fail(FRAM_ERR_USAGE, "delta_th must be >= 0");
   if (s.max_outer < 1 || s.sdsn_max < 1 || s.sdsn_fixed < 0) return fail(FRAM_ERR_USAGE, "bad caps");
   if (s.replay_len < 0 || (s.replay_len > 0 && !s.replay_passes)) return fail(FRAM_ERR_USAGE, "bad replay");
+  if (s.replay_len > s.max_outer)
+    return fail(FRAM_ERR_USAGE, "replay_len must be <= max_outer (the stats trace arrays hold max_outer entries)");
   for (int i = 0; i < s.replay_len; ++i)
     if (s.replay_passes[i] < 1) return fail(FRAM_ERR_USAGE, "replay pass counts must be >= 1");
   return FRAM_OK;
@@ -237,15 +243,24 @@ fram_status gradient(fram_ctx* h, int op, bool haveK, cudaStream_t st) {
 }
 
 // SDSN kernel choice: 4 = K4c (one cluster; FP64 n ≤ ~600, FP32 n ≤ 160), 2 = K4r (FP32 on chip,
-// n ≤ 4096), 1 = K4 (streaming).  FRAM_SDSN_STREAM forces K4, FRAM_SDSN_NOCLUSTER skips K4c (dev
-// comparison of the kernels).
+// n ≤ 4096), 1 = K4 (streaming).  Dev comparisons of the kernels build a variant library with
+// -DFRAM_DEV_FORCE_STREAM=1 or -DFRAM_DEV_NOCLUSTER=1 (tools/build_variant.sh); the product has no
+// run-time knobs.
+#ifndef FRAM_DEV_FORCE_STREAM
+#define FRAM_DEV_FORCE_STREAM 0
+#endif
+#ifndef FRAM_DEV_NOCLUSTER
+#define FRAM_DEV_NOCLUSTER 0
+#endif
+#ifndef FRAM_DEV_RES_TIMING
+#define FRAM_DEV_RES_TIMING 0
+#endif
 int sdsn_kind(const fram_ctx* h, bool f64) {
-  static const bool force_stream = getenv("FRAM_SDSN_STREAM") != nullptr;
-  static const bool no_cluster = getenv("FRAM_SDSN_NOCLUSTER") != nullptr;
-  if (force_stream) return 1;
+  if (FRAM_DEV_FORCE_STREAM) return 1;
   // K4c where it measured fastest (tools/sdsn_small_timing.py): FP64 up to its size limit (vs K4),
   // FP32 only for n ≤ 160 (with the mbarrier hand-off K4c and K4r tie at n = 256, K4r is faster above)
-  if (!no_cluster && !h->no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160)) return 4;
+  if (!FRAM_DEV_NOCLUSTER && !h->no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160))
+    return 4;
   if (!f64 && fram::sdsn_res_grid(h->n, h->num_sms) > 0) return 2;
   return 1;
 }
@@ -293,14 +308,16 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
     r.passes_out = reinterpret_cast<int*>(scal + 8);
     r.gamma_hist = h->ghist.as<double>();
     r.sdsn_out = scal;
-    static const bool timing = getenv("FRAM_RES_TIMING") != nullptr;
-    if (timing) {
+#if FRAM_DEV_RES_TIMING   // dev builds only (tools/build_variant.sh ... -DFRAM_DEV_RES_TIMING=1)
+    {
       CK(h->rdbg.ensure((size_t)h->num_sms * 24 * 8), "alloc dbg");
       r.dbg = h->rdbg.as<long long>();
       CK(cudaMemsetAsync(r.dbg, 0, (size_t)h->num_sms * 24 * 8, st), "dbg memset");
     }
+#endif
     CK(fram::launch_sdsn_resident(r, st, h->num_sms), "sdsn (on-chip) launch");
-    if (timing) {
+#if FRAM_DEV_RES_TIMING
+    {
       std::vector<long long> d((size_t)h->num_sms * 24);
       CK(cudaMemcpyAsync(d.data(), r.dbg, d.size() * 8, cudaMemcpyDeviceToHost, st), "dbg");
       CK(cudaStreamSynchronize(st), "dbg sync");
@@ -328,6 +345,7 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
       fprintf(stderr, "[res timing] rows cycles/pass g0 %.0f g1 %.0f -> SM clock %.0f / %.0f MHz\n", d[11] / np, d[12] / np,
               1e3 * d[11] / std::max(1.0, (double)d[9]), 1e3 * d[12] / std::max(1.0, (double)d[10]));
     }
+#endif
     h->launches += 2;   // flag memset + kernel
     return FRAM_OK;
   }
@@ -804,7 +822,16 @@ fram_status fram_lap(fram_handle h, const double* Nin, int32_t* perm_out, void* 
   CK(h->N.ensure((size_t)n * ld * 8), "alloc N");
   CK(h->lapw.ensure(fram::lap_work_bytes(n)), "alloc lap");
   CK(h->permd.ensure((size_t)n * 4), "alloc perm");
+  CK(h->scan.ensure(sizeof(fram::PrecondScan)), "alloc scan");
   CK(cudaMemcpy2DAsync(h->N.p, ld * 8, Nin, n * 8, n * 8, n, cudaMemcpyDefault, st), "N copy");
+  {   // a NaN would never win a comparison and leave the search without a column: reject non-finite N
+    unsigned long long* bad = reinterpret_cast<unsigned long long*>(h->scan.p);
+    CK(fram::launch_scan_finite(h->N.as<double>(), n * ld, bad, st), "scan");   // ld padding is zero
+    unsigned long long hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, 8, cudaMemcpyDeviceToHost, st), "scan readback");
+    CK(cudaStreamSynchronize(st), "scan sync");
+    if (hbad) return fail(FRAM_ERR_DATA, "N must be finite");
+  }
   CK(fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
   CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
   CK(cudaStreamSynchronize(st), "sync");

@@ -129,6 +129,7 @@ cudaError_t launch_pad_convert(double* dst, long ldd, long drows, long dcols, co
                                long rows, long cols, cudaStream_t st);
 cudaError_t launch_copy2d_f64(double* dst, long ldd, const double* src, long lds, long rows,
                               long cols, cudaStream_t st);
+cudaError_t launch_scan_finite(const double* X, long count, unsigned long long* bad, cudaStream_t st);
 cudaError_t launch_scan_nonneg(const void* X, bool f64, long n, unsigned long long* bad,
                                cudaStream_t st);
 

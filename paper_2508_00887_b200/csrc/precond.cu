@@ -181,7 +181,8 @@ cudaError_t launch_precond_apply(const void* A, const void* B, const void* K, in
   return cudaGetLastError();
 }
 
-// Standalone SDSN input check: count negative or non-finite entries of an ld-padded matrix.
+// Standalone input checks: SDSN counts negative or non-finite entries; the LAP (any real N,
+// Eq.2) counts non-finite entries only.
 template <typename T>
 __global__ void scan_nonneg_kernel(const T* X, long n, unsigned long long* bad) {
   unsigned long long cnt = 0;
@@ -193,12 +194,27 @@ __global__ void scan_nonneg_kernel(const T* X, long n, unsigned long long* bad) 
   if (cnt) atomicAdd(bad, cnt);
 }
 
+__global__ void scan_finite_kernel(const double* X, long count, unsigned long long* bad) {
+  unsigned long long cnt = 0;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < count; idx += (long)gridDim.x * blockDim.x)
+    if (!isfinite(X[idx])) ++cnt;
+  if (cnt) atomicAdd(bad, cnt);
+}
+
 cudaError_t launch_scan_nonneg(const void* X, bool f64, long n, unsigned long long* bad, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st);
   if (e != cudaSuccess) return e;
   const int blocks = 592, threads = 256;
   if (f64) scan_nonneg_kernel<double><<<blocks, threads, 0, st>>>((const double*)X, n, bad);
   else scan_nonneg_kernel<float><<<blocks, threads, 0, st>>>((const float*)X, n, bad);
+  return cudaGetLastError();
+}
+
+// `count` consecutive doubles (an ld-padded buffer whose padding is zero may be scanned whole)
+cudaError_t launch_scan_finite(const double* X, long count, unsigned long long* bad, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  scan_finite_kernel<<<592, 256, 0, st>>>(X, count, bad);
   return cudaGetLastError();
 }
 

@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
   cluster_sync();
   double m = 0.0;
   for (int k = 0; k < C; ++k) m = fmax(m, s_M[k]);
-  if (m == 0.0) {                                        // R10: all-zero ⇒ 11ᵀ/n, 0 passes
+  if (P.scale && m == 0.0) {                                        // R10 (θ-scaling on): all-zero ⇒ 11ᵀ/n, 0 passes
     for (int i = warp; i < R; i += kCWarps)
       for (int j = lane; j < n; j += 32) reinterpret_cast<T*>(P.Y)[(long)(r0 + i) * P.ld + j] = (T)(1.0 / dn);
     if (c == 0 && tid == 0) {

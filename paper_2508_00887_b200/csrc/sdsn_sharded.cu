@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kShThreads, 1) sh_pass_kernel(ShardSdsnParams 
   bool last = false;
   if (mode == 0) {
     const double m = P.recv[0];
-    if (m == 0.0) {                                              // R10: all-zero ⇒ 11ᵀ/n, 0 passes
+    if (P.scale && m == 0.0) {                                              // R10 (θ-scaling on): all-zero ⇒ 11ᵀ/n, 0 passes
       for (long i = r0; i < r1; ++i)
         for (long j = tid; j < n; j += kShThreads) Y[i * ld + j] = (T)(1.0 / dn);
       if (blockIdx.x == 0 && tid == 0) {

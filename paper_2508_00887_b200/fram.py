@@ -166,9 +166,10 @@ def _like(ref, shape, kind):
 class Handle:
     """Owns a fram_handle (fram_create / fram_destroy).  `rows` = n, or n/W for a sharded handle."""
 
-    def __init__(self, ptr, n, rows=None, rank=0, world=1):
+    def __init__(self, ptr, n, rows=None, rank=0, world=1, schedule=None):
         self.ptr = ptr
         self.n = n
+        self.schedule = schedule or Schedule()     # sizes the stats trace arrays (max_outer entries)
         self.rows = n if rows is None else rows
         self.rank = rank
         self.world = world
@@ -191,13 +192,14 @@ def fram_create(n, lam=1.0, schedule: Schedule | None = None, device=0) -> Handl
     out = C.c_void_p()
     _check(lib().fram_create(int(n), float(lam), C.byref(s), int(device), C.byref(out)))
     del keep
-    return Handle(out, int(n))
+    return Handle(out, int(n), schedule=schedule)
 
 
 def fram_set_schedule(h: Handle, schedule: Schedule):
     s, keep = schedule.to_c()
     _check(lib().fram_set_schedule(h.ptr, C.byref(s)))
     del keep
+    h.schedule = schedule
 
 
 def _stats_dict(st, nout, arrays):
@@ -213,17 +215,24 @@ def _stats_dict(st, nout, arrays):
     return d
 
 
-def fram_solve(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, X_out=None, perm_out=None,
-               max_outer=1000):
-    """Alg. 1 end to end.  Returns (status, stats, X_out, perm_out); raises FramError on errors."""
-    n = h.n
-    X_out = _like(A, (h.rows, n), "f64") if X_out is None else X_out
-    perm_out = _like(A, (n,), "i32") if perm_out is None else perm_out
-    arrays = ((C.c_int32 * max_outer)(), (C.c_double * max_outer)(), (C.c_double * max_outer)())
+def _trace_arrays(h: Handle):
+    """Host trace arrays of fram_stats, sized from the handle's schedule (the C side writes at most
+    max_outer entries; a replay longer than max_outer is rejected by check_schedule)."""
+    cap = max(1, int(h.schedule.max_outer), len(h.schedule.replay or []))
+    arrays = ((C.c_int32 * cap)(), (C.c_double * cap)(), (C.c_double * cap)())
     st = _Stats()
     st.passes_per_iter = C.cast(arrays[0], C.POINTER(C.c_int32))
     st.delta_trace = C.cast(arrays[1], C.POINTER(C.c_double))
     st.gamma_last = C.cast(arrays[2], C.POINTER(C.c_double))
+    return st, arrays
+
+
+def fram_solve(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, X_out=None, perm_out=None):
+    """Alg. 1 end to end.  Returns (status, stats, X_out, perm_out); raises FramError on errors."""
+    n = h.n
+    X_out = _like(A, (h.rows, n), "f64") if X_out is None else X_out
+    perm_out = _like(A, (n,), "i32") if perm_out is None else perm_out
+    st, arrays = _trace_arrays(h)
     status = lib().fram_solve(h.ptr, _dt_of(A), _ptr(A), _ptr(B), _ptr(K), _ptr(X0), PREC[precision],
                               _stream(stream, A), _ptr(X_out), _ptr(perm_out), C.byref(st))
     _check(status, allow_nc=True)
@@ -231,7 +240,7 @@ def fram_solve(h: Handle, A, B, K=None, X0=None, precision="bf16", stream=None, 
 
 
 def fram_solve_attributed(h: Handle, A, B, F=None, Ft=None, precision="bf16", stream=None, X_out=None,
-                          perm_out=None, max_outer=1000):
+                          perm_out=None):
     """Attributed graphs of possibly unequal size (R30): A n1×n1, B n2×n2, F n1×d, F̃ n2×d; padded to
     the handle's n; K = F F̃ᵀ on the device.  Returns (status, stats, X_out (n×n), perm_out (n1; −1 =
     matched to a padding node))."""
@@ -240,11 +249,7 @@ def fram_solve_attributed(h: Handle, A, B, F=None, Ft=None, precision="bf16", st
     d = 0 if F is None else F.shape[1]
     X_out = _like(A, (n, n), "f64") if X_out is None else X_out
     perm_out = _like(A, (n1,), "i32") if perm_out is None else perm_out
-    arrays = ((C.c_int32 * max_outer)(), (C.c_double * max_outer)(), (C.c_double * max_outer)())
-    st = _Stats()
-    st.passes_per_iter = C.cast(arrays[0], C.POINTER(C.c_int32))
-    st.delta_trace = C.cast(arrays[1], C.POINTER(C.c_double))
-    st.gamma_last = C.cast(arrays[2], C.POINTER(C.c_double))
+    st, arrays = _trace_arrays(h)
     status = lib().fram_solve_attributed(h.ptr, _dt_of(A), int(n1), int(n2), int(d), _ptr(A), _ptr(B), _ptr(F),
                                          _ptr(Ft), PREC[precision], _stream(stream, A), _ptr(X_out),
                                          _ptr(perm_out), C.byref(st))
@@ -280,7 +285,8 @@ def fram_sdsn(h: Handle, X, precision="fp32", D_out=None, stream=None, want_gamm
         else:
             D_out = np.empty_like(X)
     passes = C.c_int32(0)
-    cap = cap or 200000
+    sch = h.schedule
+    cap = cap or max(1, int(sch.sdsn_max), int(sch.sdsn_fixed))    # fram.h: double[max(sdsn_max, sdsn_fixed)]
     gh = (C.c_double * cap)() if want_gammas else None
     _check(lib().fram_sdsn(h.ptr, p, _ptr(X), _ptr(D_out), C.byref(passes),
                            C.cast(gh, C.c_void_p) if gh is not None else None, _stream(stream, X)))
@@ -326,7 +332,7 @@ def fram_create_sharded(n, lam, schedule: Schedule | None, uid: bytes, rank, wor
     _check(lib().fram_create_sharded(int(n), float(lam), C.byref(s), uid, int(rank), int(world), int(device),
                                      C.byref(out)))
     del keep
-    return Handle(out, int(n), rows=int(n) // int(world), rank=int(rank), world=int(world))
+    return Handle(out, int(n), rows=int(n) // int(world), rank=int(rank), world=int(world), schedule=schedule)
 
 
 def shard_rows(n, rank, world):

@@ -198,3 +198,17 @@ def test_fram_attributed_recovers_planted_subgraph():
     F = Ft[emb]
     out = oracle.fram_attributed(A, B, F, Ft, n2, lam=1.0, theta=10.0)
     assert np.array_equal(out["perm_attr"], emb)
+
+
+def test_matching_error_hand_computed():
+    # ½‖A − MÃMᵀ‖_F + ‖F − MF̃‖_F, (MÃMᵀ)_ij = Ã[perm i, perm j], (MF̃)_i = F̃[perm i].
+    A = np.array([[0, 1, 0], [1, 0, 1], [0, 1, 0]], float)      # path 0-1-2
+    B = np.array([[0, 1, 1], [1, 0, 0], [1, 0, 0]], float)      # star centred at 0
+    F = np.array([[1.0], [2.0], [3.0]])
+    Ft = np.array([[2.0], [1.0], [5.0]])
+    # identity: A − B has four unit entries → ½·2 = 1; F − F̃ = (−1, 1, −2) → √6
+    assert oracle.matching_error(A, B, [0, 1, 2]) == 1.0
+    assert abs(oracle.matching_error(A, B, [0, 1, 2], F, Ft) - (1.0 + np.sqrt(6.0))) <= 1e-15
+    # perm (1, 0, 2) maps the path's centre onto the star's centre: MÃMᵀ = A; F̃[perm] = (1, 2, 5)
+    assert oracle.matching_error(A, B, [1, 0, 2]) == 0.0
+    assert oracle.matching_error(A, B, [1, 0, 2], F, Ft) == 2.0

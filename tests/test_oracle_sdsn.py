@@ -156,3 +156,48 @@ def test_lap_recovers_planted_from_sdsn(rng):
     X = P * 3 + rng.random((n, n))
     D, _ = oracle.sdsn(X, 10.0)
     assert np.array_equal(lap_max(D), np.argmax(P, axis=1))
+
+
+# ---- FP32-stored SDSN (the emulated-rounding diagnostic reference) ----
+@pytest.mark.parametrize("n", [4, 8, 64, 256])
+def test_sdsn_fp32_closed_form_B_bitexact(rng, n):
+    # SDSN(P, θ=2) = P: every quantity (1/n, S/n², a, b) is a power of two for n = 2^k, so exact in FP32
+    P = random_perm_matrix(rng, n)
+    D, k = oracle.sdsn_fp32(P, 2.0)
+    assert k == 2 and np.array_equal(D, P)
+
+
+@pytest.mark.parametrize("n", [4, 32, 1024])
+def test_sdsn_fp32_uniform_input(n):
+    # X = c·11ᵀ: Y⁰ = θ/2 everywhere, a = 1/n, b = −θ/2, so Y¹ = 11ᵀ/n exactly (n = 2^k); γ₁ = 0 stops
+    # after pass 2 (R5) with 11ᵀ/n unchanged.
+    D, k, g = oracle.sdsn_fp32(np.full((n, n), 3.0), 10.0, return_gammas=True)
+    assert k == 2 and np.all(D == 1.0 / n) and g[1] == 0.0
+
+
+def test_sdsn_fp32_is_fp32_and_close_to_fp64(rng):
+    # storage is FP32 (every output value round-trips through float32), and the deviation from the FP64
+    # oracle after k passes stays within the FP32 rounding bound: each pass adds ≤ 2 roundings of
+    # relative size u32 to |Y| ≤ θ/2 and the pass map is nonexpansive ([M22]) ⇒ ≤ 2·k·u32·θ/2.
+    n, th, k = 50, 10.0, 60
+    X = random_nonneg(rng, n, "uniform").astype(np.float32).astype(np.float64)
+    D32, k32 = oracle.sdsn_fp32(X, th, sdsn_fixed=k)
+    D64, _ = oracle.sdsn(X, th, sdsn_fixed=k)
+    assert k32 == k
+    assert np.array_equal(D32, D32.astype(np.float32).astype(np.float64))
+    err = np.max(np.abs(D32 - D64))
+    assert 0 < err <= 2 * k * 2.0 ** -24 * th / 2
+    assert np.all(D32 >= 0)
+
+
+def test_dsn_fixed_one_round_is_p2_of_p1(rng):
+    # DSPFP's DSN has no θ-scaling: one round is P2(P1(X)) of the raw X.  A non-uniform X
+    # with entries far from 1/n distinguishes it from the θ-scaled SDSN.
+    n = 9
+    X = rng.random((n, n)) * 7.0
+    X[2, 3] = 40.0
+    one = oracle.p2_nonneg(oracle.p1_project(X))
+    assert np.allclose(oracle.dsn_fixed(X, 1), one, rtol=0, atol=1e-13)
+    assert np.allclose(oracle.dsn_fixed(X, 2), oracle.p2_nonneg(oracle.p1_project(one)), rtol=0, atol=1e-13)
+    Ds, _ = oracle.sdsn(X, 2.0, sdsn_fixed=1)
+    assert np.max(np.abs(Ds - one)) > 1e-3           # θ-scaled SDSN differs: the scaling is really skipped
