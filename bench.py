@@ -29,7 +29,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "FRAM iters/s & time-to-solution at n=4096; GEMM TC util %, SDSN HBM GB/s"
 UNIT = "outer iterations/s"
-WORKLOAD = "C4: BA(m=5) n=4096, 5% rewiring, X0=11^T/n, bf16-GEMM/fp32-SDSN, theta=10"
+def workload(prec):
+    sd = "fp64-SDSN" if prec == "fp64" else "fp32-SDSN"
+    return f"C4: BA(m=5) n=4096, 5% rewiring, X0=11^T/n, {prec}-GEMM/{sd}, theta=10"
+
+
+def dtype_label(prec):
+    return "f64" if prec == "fp64" else f"{prec}-gemm/f32-sdsn/f64-update"
 SCHEDULE = dict(theta=10.0, alpha=0.95, lam=1.0, gamma_th=1e-3, delta_th=1e-4, sdsn_max=1000, max_outer=100)
 
 
@@ -43,6 +49,8 @@ def parse():
     p.add_argument("--n", type=int, default=4096, help="dev override (the metric is quoted at 4096)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-extra-precisions", action="store_true",
+                   help="skip the TF32 (the paper's step-5 precision) and FP64 C4 solves reported beside the main line")
     p.add_argument("--workload", default="c4", choices=["c4", "c3", "c5"],
                    help="c4: the metric's config (n=4096, replicas across ranks); c3: 4096 keypoint instances "
                         "(n=64) split across the ranks, one CTA per instance; c5: n=16384 row-sharded across "
@@ -67,6 +75,25 @@ def peaks():
             "MEASURED_PEAKS.json"
     except Exception:
         return 6650.0, 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+
+
+# B200 nominal dense tensor rates relative to BF16 (2.25 PFLOP/s): TF32 1/2, FP16 1, FP64 40 TF/s (DMMA)
+NOMINAL_RATIO = {"bf16": 1.0, "fp16": 1.0, "tf32": 0.5, "fp64": 40.0 / 2250.0}
+
+
+def gemm_peak(prec):
+    """Sustained dense GEMM peak for the operand format: measured (profiles/measured_peaks_extra.json,
+    tools/measure_peaks.py, the same recipe as MEASURED_PEAKS.json's BF16) when present, else the BF16
+    measured sustained peak × the nominal ratio."""
+    _, _, bf16s, src = peaks()
+    if prec == "bf16":
+        return bf16s, f"{src} bf16_tflops_sustained"
+    try:
+        with open(os.path.join(ROOT, "profiles", "measured_peaks_extra.json")) as f:
+            d = json.load(f)
+        return float(d[f"{prec}_tflops_sustained"]), f"profiles/measured_peaks_extra.json {prec}_tflops_sustained"
+    except Exception:
+        return bf16s * NOMINAL_RATIO[prec], f"{src} bf16 sustained x nominal {prec}/bf16 ratio {NOMINAL_RATIO[prec]:.4g}"
 
 
 class ClockSampler:
@@ -154,10 +181,42 @@ def oracle_sample(inst, passes_per_iter, budget_s=12.0):
     float(np.linalg.norm(N_new - N) / np.linalg.norm(N_new))
     t_upd = time.perf_counter() - tu
     it = t_grad + passes_per_iter * t_pass + t_upd
-    desc = (f"FP64 NumPy oracle on the {inst.name} n={n} input: 1 gradient (2 BLAS GEMMs) {t_grad:.2f}s + {k} "
-            f"SDSN passes at {t_pass * 1e3:.1f} ms/pass (single-threaded NumPy) + 1 update {t_upd:.2f}s, timed; "
-            f"one outer iteration extrapolated to {passes_per_iter:.0f} passes/iteration")
+    desc = (f"FP64 NumPy oracle on the {inst.name} n={n} input: 1 gradient (2 BLAS GEMMs, {blas_threads()} BLAS "
+            f"threads) {t_grad:.2f}s + {k} SDSN passes at {t_pass * 1e3:.1f} ms/pass (NumPy, one core) + 1 update "
+            f"{t_upd:.2f}s, timed; one outer iteration extrapolated to {passes_per_iter:.0f} passes/iteration")
     return 1.0 / it, time.perf_counter() - t0, desc, t_pass, t_grad
+
+
+def _oracle_worker(args):
+    n, ppi, budget = args
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from synth import config_c4
+    return oracle_sample(config_c4(0, n=n), ppi, budget_s=budget)[0]
+
+
+def oracle_all_cores(n, ppi, budget_s=10.0):
+    """The oracle's SDSN pass is single-threaded NumPy, so the host's full capacity is measured the way
+    a multi-core user would get it: P = os.cpu_count() independent oracle samples in P processes at
+    once (one BLAS thread each); aggregate iterations/s = Σ of the per-process rates."""
+    import concurrent.futures as cf
+    import multiprocessing as mp
+    P = os.cpu_count() or 1
+    ctx = mp.get_context("spawn")
+    with cf.ProcessPoolExecutor(max_workers=P, mp_context=ctx) as ex:
+        rates = list(ex.map(_oracle_worker, [(n, ppi, budget_s)] * P))
+    return sum(rates), P
+
+
+def cpu_baseline_entry(inst, ppi, budget_s, all_cores=True):
+    v, secs, desc, t_pass, _ = oracle_sample(inst, ppi, budget_s=budget_s)
+    out = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+           "sample": desc + " (cores = 1: the SDSN passes, >99% of the oracle's time, use one core)"}
+    if all_cores:
+        agg, P = oracle_all_cores(inst.n, ppi, budget_s=min(budget_s, 8.0))
+        out["all_cores"] = {"value": agg, "unit": UNIT, "cores": P,
+                            "sample": f"{P} independent oracle samples of the same workload run concurrently in "
+                                      f"{P} processes (1 BLAS thread each); aggregate outer iterations/s"}
+    return out
 
 
 def run_reference(args):
@@ -166,23 +225,22 @@ def run_reference(args):
         return 0
     from synth import config_c4
     inst = config_c4(0, n=args.n)
-    ppi = float(SCHEDULE["sdsn_max"])    # at C4 the 1000-pass cap binds on every call after t=1 (R3, [M16])
+    ppi = float(SCHEDULE["sdsn_max"])    # at C4 the 1000-pass cap binds on every call (R3, [M16], golden)
     for _ in range(args.warmup):
         oracle_sample(inst, ppi, budget_s=4.0)
     vals, secs = [], []
     desc = ""
     for _ in range(args.steps):
-        v, s, desc, _, _ = oracle_sample(inst, ppi, budget_s=8.0)
+        v, s_, desc, _, _ = oracle_sample(inst, ppi, budget_s=8.0)
         vals.append(v)
-        secs.append(s)
+        secs.append(s_)
     value = statistics.median(vals)
-    cores = blas_threads()
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(secs),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded C4 generator; SNAP Facebook-ego stand-in)",
-            "config": {"workload": WORKLOAD, "n": args.n, "schedule": SCHEDULE, "seed": 0},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "config": {"workload": workload(args.precision), "n": args.n, "schedule": SCHEDULE, "seed": 0},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -212,47 +270,57 @@ def run_ours(args):
     h = fb.fram_create(n, lam=SCHEDULE["lam"], schedule=sch, device=local)
     X = torch.empty((n, n), dtype=torch.float64, device=dev)
     perm = torch.empty((n,), dtype=torch.int32, device=dev)
-    for _ in range(args.warmup):
-        fb.fram_solve(h, A, B, precision=args.precision, X_out=X, perm_out=perm)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)     # 256 MiB > 126 MB L2
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    sampler = ClockSampler(local)
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    barrier()
-    torch.cuda.synchronize()
-    sampler.start()
-    stats = []
-    for k in range(args.steps):
-        flush.fill_(float(k))                                         # L2 flush, outside the events
-        ev[k][0].record()
-        st, s, _, _ = fb.fram_solve(h, A, B, precision=args.precision, X_out=X, perm_out=perm)
-        ev[k][1].record()
-        stats.append(s)
-    torch.cuda.synchronize()
-    barrier()
-    clocks = sampler.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    tot_ms = sum(step_ms)
-    iters = sum(s["outer_iters"] for s in stats)
-    passes = sum(s["total_passes"] for s in stats)
-    launches = sum(s["kernel_launches"] for s in stats)
-    ms_sdsn = sum(s["ms_sdsn"] for s in stats)
-    ms_gemm = sum(s["ms_gemm"] for s in stats)
-    ms_lap = sum(s["ms_lap"] for s in stats)
-    acc = float((perm.cpu().numpy() == inst.perm_true).mean())
-    if world > 1:
-        t = torch.tensor([tot_ms], dtype=torch.float64, device=dev)
+    def timed(prec, steps, warmup, sampler=None):
+        """`steps` device-timed solves (CUDA events on the current stream, L2 flushed before each)."""
+        for _ in range(warmup):
+            fb.fram_solve(h, A, B, precision=prec, X_out=X, perm_out=perm)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        barrier()
+        torch.cuda.synchronize()
+        if sampler:
+            sampler.start()
+        stats = []
+        for k in range(steps):
+            flush.fill_(float(k))                                         # L2 flush, outside the events
+            ev[k][0].record()
+            st, s_, _, _ = fb.fram_solve(h, A, B, precision=prec, X_out=X, perm_out=perm)
+            ev[k][1].record()
+            stats.append(s_)
+        torch.cuda.synchronize()
+        barrier()
+        clocks = sampler.stop() if sampler else None
+        return [a.elapsed_time(b) for a, b in ev], stats, clocks
+
+    def allmax(v):
+        if world == 1:
+            return float(v)
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        tot_ms_all = float(t.item())
-        it = torch.tensor([iters], dtype=torch.float64, device=dev)
-        dist.all_reduce(it, op=dist.ReduceOp.SUM)
-        iters_all = float(it.item())
-    else:
-        tot_ms_all, iters_all = tot_ms, float(iters)
+        return float(t.item())
+
+    def allsum(v):
+        if world == 1:
+            return float(v)
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    step_ms, stats, clocks = timed(args.precision, args.steps, args.warmup, ClockSampler(local))
+    tot_ms = sum(step_ms)
+    iters = sum(s_["outer_iters"] for s_ in stats)
+    passes = sum(s_["total_passes"] for s_ in stats)
+    launches = sum(s_["kernel_launches"] for s_ in stats)
+    ms_sdsn = sum(s_["ms_sdsn"] for s_ in stats)
+    ms_gemm = sum(s_["ms_gemm"] for s_ in stats)
+    ms_lap = sum(s_["ms_lap"] for s_ in stats)
+    acc = float((perm.cpu().numpy() == inst.perm_true).mean())
+    tot_ms_all, iters_all = allmax(tot_ms), allsum(iters)
     value = iters_all / (tot_ms_all / 1e3)
 
     # ---- e2e: same solve through the C ABI with pinned HOST buffers (H2D/D2H inside the region)
@@ -271,19 +339,13 @@ def run_ours(args):
             flush.fill_(float(k))
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            _, s, _, _ = fb.fram_solve(h, Ah, Bh, precision=args.precision, X_out=Xh, perm_out=ph,
-                                       stream=torch.cuda.current_stream(dev))
+            _, s_, _, _ = fb.fram_solve(h, Ah, Bh, precision=args.precision, X_out=Xh, perm_out=ph,
+                                        stream=torch.cuda.current_stream(dev))
             b.record()
             b.synchronize()
             e_ms += a.elapsed_time(b)
-            e_it += s["outer_iters"]
-        if world > 1:
-            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t.item())
-            it = torch.tensor([e_it], dtype=torch.float64, device=dev)
-            dist.all_reduce(it, op=dist.ReduceOp.SUM)
-            e_it = float(it.item())
+            e_it += s_["outer_iters"]
+        e_ms, e_it = allmax(e_ms), allsum(e_it)
         e2e = {"value": e_it / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(Ah.nbytes + Bh.nbytes),
                "d2h_bytes_per_step": int(Xh.nbytes + ph.nbytes)}
 
@@ -294,7 +356,6 @@ def run_ours(args):
     passes_per_launch = passes / sdsn_launches
     esz = 8.0 if args.precision == "fp64" else 4.0            # SDSN iterate: FP64 in FP64 mode, else FP32
     bytes_per_launch = 2.0 * esz * n * n * passes_per_launch  # algorithmic: Y read + write per pass
-    hbm_equiv = bytes_per_launch / avg_launch_s / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "sdsn_traffic.json")
     if os.path.exists(tpath):
@@ -324,9 +385,15 @@ def run_ours(args):
                                "FP32 lanes, the max overlapped on the ALU pipe; B200_PROFILING.md unit counts, "
                                "FADD2 rate measured by tools/pipe_probe.cu)",
                 "algorithmic_flops_per_launch": 5.0 * n * n * passes_per_launch,
-                "hbm_equivalent": {"achieved_gbs": hbm_equiv, "peak_gbs": hbm, "frac": hbm_equiv / hbm,
-                                   "note": "algorithmic 8n^2 B/pass over the launch time; the iterate never leaves the chip"}}
+                "hbm_note": "the iterate never leaves the chip, so the north star's >=70%-of-HBM SDSN target does "
+                            "not apply to K4r: its DRAM traffic is the one G load + D store per launch",
+                "dram": {"bytes_per_launch": traffic,
+                         "achieved_gbs": (traffic / avg_launch_s / 1e9) if traffic else None,
+                         "frac_of_hbm": (traffic / avg_launch_s / 1e9 / hbm) if traffic else None,
+                         "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum per launch "
+                                   "(profiles/sdsn_traffic.json) over the live launch time"}}
     else:
+        hbm_equiv = bytes_per_launch / avg_launch_s / 1e9
         roof = {"kernel": f"sdsn_kernel<{'double' if esz == 8 else 'float'}> (K4, streaming through L2/HBM)",
                 "bound": "hbm", "achieved": hbm_equiv,
                 "peak": hbm, "unit": "GB/s", "frac": hbm_equiv / hbm, "traffic": traffic, "peak_source": psrc,
@@ -338,32 +405,61 @@ def run_ours(args):
                             "note": "ncu DRAM bytes per launch (profiles/sdsn_traffic.json) over the launch time"}
     roof.update({"passes_per_launch": passes_per_launch, "ms_per_launch": avg_launch_s * 1e3,
                  "us_per_pass": avg_launch_s * 1e6 / passes_per_launch, "share_of_step": ms_sdsn / tot_ms})
-    gemm_tflops = 4.0 * n ** 3 * iters / (ms_gemm / 1e3) / 1e12 if ms_gemm > 0 else None
+
+    def gemm_entry(prec, ms_gemm_, iters_, steps_):
+        tfl = 4.0 * n ** 3 * iters_ / (ms_gemm_ / 1e3) / 1e12 if ms_gemm_ > 0 else None
+        pk, src = gemm_peak(prec)
+        return {"tflops": tfl, "peak_tflops": pk, "peak_source": src, "frac_of_sustained": (tfl or 0) / pk,
+                "ms_per_step": ms_gemm_ / steps_, "operand_format": prec}
+
+    # ---- the paper's precisions beside the headline (TF32 = step 5 of Alg.1; FP64 = "GPU-FP64")
+    extra = {}
+    if not args.no_extra_precisions:
+        for prec in ("tf32", "fp64"):
+            if prec == args.precision:
+                continue
+            sm_, st_, _ = timed(prec, 2, 1)
+            it_ = sum(x["outer_iters"] for x in st_)
+            ms_ = allmax(sum(sm_))
+            ms_s = sum(x["ms_sdsn"] for x in st_)
+            ps_ = sum(x["total_passes"] for x in st_)
+            extra[prec] = {"value": allsum(it_) / (ms_ / 1e3), "unit": UNIT, "time_to_solution_ms": statistics.median(sm_),
+                           "outer_iters_per_solve": it_ / 2, "mean_passes_per_iter": ps_ / it_,
+                           "accuracy": float((perm.cpu().numpy() == inst.perm_true).mean()),
+                           "sdsn_us_per_pass": 1e3 * ms_s / ps_, "dtype": dtype_label(prec),
+                           "gemm": gemm_entry(prec, sum(x["ms_gemm"] for x in st_), it_, 2),
+                           "lap_ms_per_step": sum(x["ms_lap"] for x in st_) / 2,
+                           "steps": 2, "warmup": 1}
+            if prec == "fp64":
+                # the streaming FP64 SDSN (K4) against the HBM copy peak: algorithmic 16n^2 B per pass
+                extra[prec]["sdsn_algorithmic_gbs"] = 16.0 * n * n * ps_ / (ms_s / 1e3) / 1e9
+                extra[prec]["sdsn_algorithmic_frac_of_hbm"] = extra[prec]["sdsn_algorithmic_gbs"] / hbm
+        if "fp64" in extra:
+            extra["mixed_vs_fp64_time_to_solution"] = extra["fp64"]["time_to_solution_ms"] / statistics.median(step_ms)
 
     line = None
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms_all / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "bf16-gemm/f32-sdsn/f64-update"
-                if args.precision != "fp64" else "f64",
+                "scaling": "weak", "vs_baseline": None, "dtype": dtype_label(args.precision),
                 "data": "synthetic (seeded C4 generator; SNAP Facebook-ego stand-in)",
-                "config": {"workload": WORKLOAD, "n": n, "precision": args.precision, "schedule": SCHEDULE,
-                           "seed": "rank", "replicas": world, "l2": "flushed between steps (256 MiB write)",
+                "config": {"workload": workload(args.precision), "n": n, "precision": args.precision,
+                           "schedule": SCHEDULE, "seed": "rank", "replicas": world,
+                           "l2": "flushed between steps (256 MiB write)",
                            "parallelism": f"{world} independent replicas (C4 does not shard, SURVEY 8(e))"},
                 "time_to_solution_ms": statistics.median(step_ms),
                 "outer_iters_per_solve": iters / args.steps, "mean_passes_per_iter": passes / iters,
                 "accuracy": acc,
                 "roofline": roof,
-                "gemm": {"tflops": gemm_tflops, "peak_bf16": bf16s, "frac_of_sustained": (gemm_tflops or 0) / bf16s,
-                         "ms_per_step": ms_gemm / args.steps},
+                "gemm": gemm_entry(args.precision, ms_gemm, iters, args.steps),
                 "lap_ms_per_step": ms_lap / args.steps,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clocks}
+        if extra:
+            line["precisions"] = extra
     if world > 1:
         dist.barrier()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        mean_ppi = passes / iters
-        v, secs, desc, _, _ = oracle_sample(inst, mean_ppi, budget_s=15.0)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": blas_threads(), "kind": "oracle", "sample": desc}
+        line["cpu_baseline"] = cpu_baseline_entry(inst, passes / iters, budget_s=15.0)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -432,7 +528,7 @@ def run_c5(args):
         line = {"metric": METRIC, "value": iters / (tot_ms / 1e3), "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "bf16-gemm/f32-sdsn/f64-update", "data": "synthetic (seeded C5 generator)",
+                "dtype": dtype_label(args.precision), "data": "synthetic (seeded C5 generator)",
                 "config": {"workload": "C5: weighted ER(p=0.01) n=16384, BF16 storage, 5% rewiring, rows sharded",
                            "n": n, "precision": args.precision, "schedule": dict(SCHEDULE, max_outer=sch.max_outer),
                            "parallelism": f"row-sharded over {world} rank(s) (NCCL)"},

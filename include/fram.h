@@ -172,6 +172,17 @@ FRAM_API fram_status fram_create_sharded(int64_t n, double lambda, const fram_sc
                                 const uint8_t id[128], int rank, int world, int device,
                                 fram_handle* out);
 
+/* Virtual-shard group (test harness for the W > 1 sharded path on ONE GPU; SURVEY §4 L-d): a handle
+ * whose fram_solve runs `world` ranks of the row-sharded solve (exactly the code of a real sharded
+ * handle: row-block GEMMs with the K-blocked operand, K4s SDSN, row-block update, LAP on the gathered
+ * N), one host thread and CUDA stream per rank, with the NCCL collectives replaced by fixed-order
+ * (rank 0..W−1) device sums and copies between the ranks' buffers.  fram_solve on this handle takes
+ * the FULL n×n A, B, K, X0 and X_out (rank r works on rows [r·n/W, (r+1)·n/W)); perm_out and stats
+ * come from rank 0.  world ∈ [1, 16], n % world == 0 (mixed precision: (n/world) % 64 == 0).
+ * fram_sdsn / fram_gradient / fram_lap / batched / attributed calls are FRAM_ERR_USAGE on it. */
+FRAM_API fram_status fram_create_sharded_virtual(int64_t n, double lambda, const fram_schedule* s, int world,
+                                                int device, fram_handle* out);
+
 /* ---- test entry points (parity harness) ----------------------------------------------------
  * fram_sdsn: one SDSN call (Alg.2) on a nonnegative n×n X.  p = FRAM_PREC_FP64: X and
  *   D_out are FP64; any other p: FP32.  Uses the handle's θ, γ_th, sdsn_max, sdsn_fixed and the

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/fram.h"
@@ -77,6 +78,17 @@ struct fram_ctx {
   fram::BatchedWs bws;
   // sharded
   fram::ShardCtx* shard = nullptr;
+  // virtual-shard group (fram_create_sharded_virtual): W rank sub-handles on this GPU, one host thread
+  // and stream each; this handle only dispatches
+  std::vector<fram_ctx*> vsub;
+  std::vector<cudaStream_t> vstreams;
+  fram::VGroup* vgroup = nullptr;
+  // sharded SDSN: a chunk of passes (pass kernel, reduce, finish, all-reduce) captured once as a CUDA
+  // graph and relaunched (NCCL communicators only; see sharded_solve)
+  cudaGraphExec_t sh_graph = nullptr;
+  cudaStream_t sh_cap_stream = nullptr;
+  bool sh_graph_off = false;        // capture failed once here: plain launches from then on
+  unsigned char sh_graph_key[sizeof(fram::ShardSdsnParams) + 8] = {};
 };
 
 namespace {
@@ -491,17 +503,58 @@ fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, con
     CK(cudaMemsetAsync(sp.state, 0, sizeof(fram::ShardSdsnState), st), "state reset");
     CK(fram::launch_sdsn_sh_max(sp, f64, st, h->num_sms), "sdsn max");
     if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, 1, true, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
-    CK(fram::launch_sdsn_sh_sweep(sp, f64, 0, 0, st, h->num_sms), "sdsn scale");
+    CK(fram::prepare_sdsn_sh(sp, f64, h->num_sms), "sdsn prepare");
+    CK(fram::launch_sdsn_sh_sweep(sp, f64, 0, st, h->num_sms), "sdsn scale");
     if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
     h->launches += 5;
     const int cap = std::max(1, sp.sdsn_fixed > 0 ? sp.sdsn_fixed : sch.sdsn_max);
-    constexpr int kChunk = 16;                         // passes queued between host polls of `done`
+    // Passes are queued kChunk at a time between host polls of `done` (passes after the last are no-ops).
+    // Every pass is the same launch sequence (the pass index lives on the device), so with an NCCL
+    // communicator a chunk is captured once as a CUDA graph — kernels and ncclAllReduce — and relaunched:
+    // one host call per chunk instead of 4 per pass.  Virtual shards synchronise their collectives on
+    // the host and keep the plain launches.
+    constexpr int kChunk = 16;
+    bool use_graph = !fram::shard_is_virtual(sh) && !h->sh_graph_off;
+    if (use_graph) {
+      unsigned char key[sizeof(h->sh_graph_key)] = {};
+      memcpy(key, &sp, sizeof(sp));
+      key[sizeof(sp)] = f64 ? 1 : 2;
+      if (!h->sh_graph || memcmp(key, h->sh_graph_key, sizeof(key)) != 0) {
+        if (h->sh_graph) { cudaGraphExecDestroy(h->sh_graph); h->sh_graph = nullptr; }
+        if (!h->sh_cap_stream) CK(cudaStreamCreateWithFlags(&h->sh_cap_stream, cudaStreamNonBlocking), "stream create");
+        CK(fram::prepare_sdsn_sh(sp, f64, h->num_sms), "sdsn prepare");
+        cudaGraph_t gr = nullptr;
+        CK(cudaStreamBeginCapture(h->sh_cap_stream, cudaStreamCaptureModeThreadLocal), "graph capture begin");
+        bool ok = true;
+        for (int p = 0; p < kChunk && ok; ++p) {
+          ok = fram::launch_sdsn_sh_sweep(sp, f64, 1, h->sh_cap_stream, h->num_sms) == cudaSuccess;
+          ok = ok && fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, h->sh_cap_stream, &err) == FRAM_OK;
+        }
+        const cudaError_t ce = cudaStreamEndCapture(h->sh_cap_stream, &gr);
+        cudaError_t ie = cudaErrorUnknown;
+        if (ok && ce == cudaSuccess) ie = cudaGraphInstantiate(&h->sh_graph, gr, 0);
+        if (gr) cudaGraphDestroy(gr);
+        if (ie == cudaSuccess) {
+          memcpy(h->sh_graph_key, key, sizeof(key));
+        } else {                                       // e.g. a collective library that cannot be captured
+          cudaGetLastError();
+          h->sh_graph = nullptr;
+          h->sh_graph_off = true;
+          use_graph = false;
+        }
+      }
+    }
     for (int p0 = 0; p0 < cap; p0 += kChunk) {
-      for (int p = p0; p < std::min(cap, p0 + kChunk); ++p) {
-        CK(fram::launch_sdsn_sh_sweep(sp, f64, 1, p, st, h->num_sms), "sdsn pass");
-        if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK)
-          return FRAM_ERR_NCCL;
-        h->launches += 3;
+      if (use_graph) {
+        CK(cudaGraphLaunch(h->sh_graph, st), "graph launch");
+        h->launches += 3 * kChunk;
+      } else {
+        for (int p = p0; p < std::min(cap, p0 + kChunk); ++p) {
+          CK(fram::launch_sdsn_sh_sweep(sp, f64, 1, st, h->num_sms), "sdsn pass");
+          if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK)
+            return FRAM_ERR_NCCL;
+          h->launches += 3;
+        }
       }
       CK(cudaMemcpyAsync(&hstate, sp.state, sizeof(hstate), cudaMemcpyDeviceToHost, st), "state readback");
       CK(cudaStreamSynchronize(st), "state sync");
@@ -576,6 +629,45 @@ fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, con
   return FRAM_OK;
 }
 
+// Virtual-shard group solve: rank r's thread runs the unchanged sharded_solve on row block r of the
+// caller's full n×n inputs (A, K, X0 and X_out are sliced by rows; Ã is shared), with the collectives
+// served by the group (sharded.cu).  Rank 0 writes perm_out and the stats.
+fram_status group_solve(fram_ctx* g, int dt, const void* A, const void* B, const void* K, const double* X0, int op,
+                        cudaStream_t caller, double* X_out, int32_t* perm_out, fram_stats* stats) {
+  const int W = (int)g->vsub.size();
+  const long n = g->n, m = n / W;
+  CK(cudaStreamSynchronize(caller), "caller stream sync");        // inputs produced on the caller's stream
+  std::vector<fram_status> st(W, FRAM_OK);
+  std::vector<std::string> msg(W);
+  const size_t es = dt_size(dt);
+  auto run = [&](int r) {
+    fram_ctx* h = g->vsub[r];
+    fram_status s0 = set_device(h);
+    if (s0 == FRAM_OK) {
+      const size_t off = (size_t)r * m * n;
+      s0 = sharded_solve(h, dt, static_cast<const char*>(A) + off * es, B,
+                         K ? static_cast<const char*>(K) + off * es : nullptr, X0 ? X0 + off : nullptr, op,
+                         g->vstreams[r], X_out ? X_out + off : nullptr, r == 0 ? perm_out : nullptr,
+                         r == 0 ? stats : nullptr);
+    }
+    st[r] = s0;
+    if (s0 != FRAM_OK && s0 != FRAM_NOT_CONVERGED) {
+      msg[r] = g_err;
+      fram::vgroup_abort(g->vgroup);             // release ranks waiting in a collective
+    }
+  };
+  std::vector<std::thread> th;
+  for (int r = 1; r < W; ++r) th.emplace_back(run, r);
+  run(0);
+  for (auto& t : th) t.join();
+  for (int r = 0; r < W; ++r)                    // the first rank's own error (not an abort it caused)
+    if (st[r] != FRAM_OK && st[r] != FRAM_NOT_CONVERGED && st[r] != FRAM_ERR_NCCL) return fail(st[r], msg[r]);
+  for (int r = 0; r < W; ++r)
+    if (st[r] != FRAM_OK && st[r] != FRAM_NOT_CONVERGED) return fail(st[r], msg[r]);
+  if (st[0] == FRAM_NOT_CONVERGED) g_err = "max_outer reached without delta <= delta_th";
+  return st[0];
+}
+
 }  // namespace
 
 extern "C" {
@@ -607,12 +699,18 @@ fram_status fram_set_schedule(fram_handle h, const fram_schedule* s) {
   h->replay.assign(s->replay_passes, s->replay_passes + s->replay_len);
   h->sched = *s;
   h->sched.replay_passes = h->replay.empty() ? nullptr : h->replay.data();
+  for (fram_ctx* sub : h->vsub) fram_set_schedule(sub, s);
   return FRAM_OK;
 }
 
 void fram_destroy(fram_handle h) {
   if (!h) return;
   cudaSetDevice(h->device);
+  for (fram_ctx* sub : h->vsub) fram_destroy(sub);
+  for (cudaStream_t s : h->vstreams) cudaStreamDestroy(s);
+  if (h->sh_graph) cudaGraphExecDestroy(h->sh_graph);
+  if (h->sh_cap_stream) cudaStreamDestroy(h->sh_cap_stream);
+  fram::vgroup_destroy(h->vgroup);
   DevBuf* bufs[] = {&h->Aq, &h->BqT, &h->Kq, &h->N, &h->Nq, &h->UT, &h->Y, &h->colpart, &h->Spart, &h->Mpart,
                     &h->cvec, &h->bar, &h->scal, &h->ghist, &h->upd, &h->lapw, &h->permd, &h->stA, &h->stB,
                     &h->stK, &h->stX0, &h->stX, &h->scan, &h->rcolpart, &h->rbvec, &h->rflags, &h->rdbg, &h->shUT, &h->shUblk, &h->shRsum,
@@ -636,6 +734,9 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (!A || !B) return fail(FRAM_ERR_USAGE, "A and B are required");
+  if (!h->vsub.empty())
+    return group_solve(h, (int)dt, A, B, K, X0, (int)p, reinterpret_cast<cudaStream_t>(stream), X_out, perm_out,
+                       stats);
   if (h->shard)
     return sharded_solve(h, (int)dt, A, B, K, X0, (int)p, reinterpret_cast<cudaStream_t>(stream), X_out, perm_out,
                          stats);
@@ -753,7 +854,7 @@ fram_status fram_sdsn(fram_handle h, fram_precision p, const void* X, void* D_ou
                       double* gamma_hist, void* stream) {
   fram_status s0 = common_checks(h, 0, p);
   if (s0 != FRAM_OK) return s0;
-  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  if (h->shard || !h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   if (!X || !D_out || !passes) return fail(FRAM_ERR_USAGE, "X, D_out and passes are required");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const bool f64 = (p == FRAM_PREC_FP64);
@@ -788,7 +889,7 @@ fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, const voi
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (!A || !B || !Nin || !G_out) return fail(FRAM_ERR_USAGE, "A, B, N and G_out are required");
-  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  if (h->shard || !h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const int op = prec_to_op(p);
   const long n = h->n, ld = h->ld;
@@ -815,7 +916,7 @@ fram_status fram_gradient(fram_handle h, fram_dtype dt, const void* A, const voi
 fram_status fram_lap(fram_handle h, const double* Nin, int32_t* perm_out, void* stream) {
   fram_status s0 = common_checks(h, 0, FRAM_PREC_FP64);
   if (s0 != FRAM_OK) return s0;
-  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  if (h->shard || !h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   if (!Nin || !perm_out) return fail(FRAM_ERR_USAGE, "N and perm_out are required");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   const long n = h->n, ld = h->ld;
@@ -844,7 +945,7 @@ fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype dt, cons
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (batch < 0 || !A || !B) return fail(FRAM_ERR_USAGE, "bad batch arguments");
-  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  if (h->shard || !h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   std::string err;
   fram_status s = fram::batched_solve(h->bws, h->n, h->lambda, h->sched, batch, (int)dt, A, B, K, X0, (int)p,
                                       reinterpret_cast<cudaStream_t>(stream), X_out, perm_out, status_out, stats,
@@ -858,7 +959,7 @@ fram_status fram_solve_attributed(fram_handle h, fram_dtype dt, int64_t n1, int6
                                   double* X_out, int32_t* perm_out, fram_stats* stats) {
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
-  if (h->shard) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  if (h->shard || !h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
   const long m = h->n;
   if (!A || !B || n1 < 1 || n2 < 1 || n1 > m || n2 > m) return fail(FRAM_ERR_USAGE, "need 1 <= n1, n2 <= handle n");
   if ((F == nullptr) != (Ft == nullptr) || (F && d < 1)) return fail(FRAM_ERR_USAGE, "F and Ft go together, d >= 1");
@@ -907,6 +1008,40 @@ fram_status fram_solve_attributed(fram_handle h, fram_dtype dt, int64_t n1, int6
     CK(cudaStreamSynchronize(st), "perm sync");
   }
   return so;
+}
+
+fram_status fram_create_sharded_virtual(int64_t n, double lambda, const fram_schedule* s, int world, int device,
+                                        fram_handle* out) {
+  if (!out) return fail(FRAM_ERR_USAGE, "null out");
+  *out = nullptr;
+  if (world < 1 || world > 16) return fail(FRAM_ERR_USAGE, "world must be in [1, 16]");
+  if (n < 1 || n % world != 0) return fail(FRAM_ERR_USAGE, "n % world != 0");
+  fram_status st = fram_create(n, lambda, s, device, out);
+  if (st != FRAM_OK) return st;
+  fram_handle g = *out;
+  std::string err;
+  st = set_device(g);
+  if (st == FRAM_OK) {
+    g->vgroup = fram::vgroup_create(world, &err);
+    if (!g->vgroup) st = fail(FRAM_ERR_CUDA, err);
+  }
+  for (int r = 0; st == FRAM_OK && r < world; ++r) {
+    fram_handle sub = nullptr;
+    st = fram_create(n, lambda, s, device, &sub);
+    if (st != FRAM_OK) break;
+    g->vsub.push_back(sub);
+    sub->dev_checked = g->dev_checked;
+    sub->num_sms = g->num_sms;
+    fram::shard_create_virtual(&sub->shard, g->vgroup, r);
+    cudaStream_t cs = nullptr;
+    if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) { st = fail(FRAM_ERR_CUDA, "stream create"); break; }
+    g->vstreams.push_back(cs);
+  }
+  if (st != FRAM_OK) {
+    fram_destroy(g);
+    *out = nullptr;
+  }
+  return st;
 }
 
 fram_status fram_get_unique_id(uint8_t id[128]) {

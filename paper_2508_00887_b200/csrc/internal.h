@@ -54,7 +54,8 @@ cudaError_t launch_sdsn_resident(const ResParams& p, cudaStream_t st, int num_sm
 
 // ---- K4s: SDSN on a row block for the sharded solve (per-pass kernels + host NCCL all-reduce) ----
 struct ShardSdsnState {
-  int done, done_pending, passes, _pad;
+  int done, done_pending, passes, pass;   // `pass`: index of the next SDSN pass (advanced on the device,
+                                          // so every pass is the same launch sequence: CUDA-graph friendly)
   double gamma_last, maxx, S_last;
 };
 struct ShardSdsnParams {
@@ -72,10 +73,11 @@ struct ShardSdsnParams {
 int sdsn_sh_grid(long rows, int num_sms, bool f64);
 size_t sdsn_sh_smem(long ld, bool f64, long rows_max);
 cudaError_t launch_sdsn_sh_max(const ShardSdsnParams& p, bool f64, cudaStream_t st, int num_sms);
-// mode 0: scale sweep (after the max all-reduce), mode 1: pass `pass`; both end with the local
-// column/mass reduction into p.send (the caller all-reduces send → recv)
-cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, int pass, cudaStream_t st,
-                                 int num_sms);
+// mode 0: scale sweep (after the max all-reduce), mode 1: the next pass (index state->pass, advanced
+// on the device); both end with the local column/mass reduction into p.send (the caller all-reduces
+// send → recv).  prepare_sdsn_sh sets the kernels' shared-memory limits (call before graph capture).
+cudaError_t prepare_sdsn_sh(const ShardSdsnParams& p, bool f64, int num_sms);
+cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, cudaStream_t st, int num_sms);
 
 // ---- K1: preconditioning (Alg.1 steps 2-3) ------------------------------------
 // in_dt: 0 f64, 1 f32, 2 bf16.  op: 0 f64, 1 tf32 (stored f32), 2 bf16, 3 fp16.

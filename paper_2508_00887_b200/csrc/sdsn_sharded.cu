@@ -51,13 +51,14 @@ __global__ void sh_max_kernel(const T* __restrict__ Y, long rows, long n, long l
 // One sweep over the CTA's rows.  mode 0: scale (y ← fl(s·y), s = (θ/2)/m from recv[0]; m = 0 ⇒
 // 11ᵀ/n and done); mode 1: SDSN pass p.  Column partials in shared memory (one owner per column).
 template <typename T>
-__global__ void __launch_bounds__(kShThreads, 1) sh_pass_kernel(ShardSdsnParams P, int mode, int p) {
+__global__ void __launch_bounds__(kShThreads, 1) sh_pass_kernel(ShardSdsnParams P, int mode) {
   using VT = typename V4<T>::t;
   constexpr int W = V4<T>::W;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ double s_w[kShThreads / 32];
   ShardSdsnState* st = P.state;
   if (st->done) return;
+  const int p = st->pass;                                        // pass index (mode 1), device-side
   const long n = P.n, ld = P.ld, rows = P.rows;
   T* s_col = reinterpret_cast<T*>(dsm);                          // [ld] column partials
   T* s_b = s_col + ld;                                           // [ld] b_j = −c_j/n (FP32 mode only)
@@ -211,8 +212,10 @@ __global__ void sh_reduce_kernel(ShardSdsnParams P, int nctas) {
   }
 }
 
-__global__ void sh_finish_kernel(ShardSdsnState* st) {
+__global__ void sh_finish_kernel(ShardSdsnState* st, int mode) {
+  if (st->done) return;
   if (st->done_pending) st->done = 1;
+  if (mode == 1) st->pass += 1;
 }
 
 }  // namespace
@@ -238,21 +241,24 @@ cudaError_t launch_sdsn_sh_max(const ShardSdsnParams& p, bool f64, cudaStream_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, int pass, cudaStream_t st, int num_sms) {
+cudaError_t prepare_sdsn_sh(const ShardSdsnParams& p, bool f64, int num_sms) {
+  const int g = sdsn_sh_grid(p.rows, num_sms, f64);
+  const size_t sm = sdsn_sh_smem(p.ld, f64, (p.rows + g - 1) / g + 1);
+  return f64 ? cudaFuncSetAttribute(sh_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm)
+             : cudaFuncSetAttribute(sh_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+}
+
+cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, cudaStream_t st, int num_sms) {
   const int g = sdsn_sh_grid(p.rows, num_sms, f64);
   const size_t sm = sdsn_sh_smem(p.ld, f64, (p.rows + g - 1) / g + 1);
   if (f64) {
-    cudaError_t e = cudaFuncSetAttribute(sh_pass_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    sh_pass_kernel<double><<<g, kShThreads, sm, st>>>(p, mode, pass);
+    sh_pass_kernel<double><<<g, kShThreads, sm, st>>>(p, mode);
     sh_reduce_kernel<double><<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(p, g);
   } else {
-    cudaError_t e = cudaFuncSetAttribute(sh_pass_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    sh_pass_kernel<float><<<g, kShThreads, sm, st>>>(p, mode, pass);
+    sh_pass_kernel<float><<<g, kShThreads, sm, st>>>(p, mode);
     sh_reduce_kernel<float><<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(p, g);
   }
-  sh_finish_kernel<<<1, 1, 0, st>>>(p.state);
+  sh_finish_kernel<<<1, 1, 0, st>>>(p.state, mode);
   return cudaGetLastError();
 }
 

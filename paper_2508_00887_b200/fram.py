@@ -24,7 +24,7 @@ FLAG_TRACE, FLAG_CHECK_SYMMETRY, FLAG_NO_THETA_SCALE, FLAG_TIME_PHASES = 1, 2, 4
 
 EXPORTED = ["fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_destroy",
             "fram_last_error", "fram_get_unique_id", "fram_create_sharded", "fram_sdsn", "fram_gradient",
-            "fram_lap", "fram_abi_version", "fram_build_info", "fram_solve_attributed"]
+            "fram_lap", "fram_abi_version", "fram_build_info", "fram_solve_attributed", "fram_create_sharded_virtual"]
 
 
 class FramError(RuntimeError):
@@ -95,6 +95,7 @@ def lib():
     L.fram_get_unique_id.argtypes = [C.c_char_p]
     L.fram_create_sharded.argtypes = [i64, dbl, C.POINTER(_Schedule), C.c_char_p, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(vp)]
+    L.fram_create_sharded_virtual.argtypes = [i64, dbl, C.POINTER(_Schedule), C.c_int, C.c_int, C.POINTER(vp)]
     L.fram_sdsn.argtypes = [vp, C.c_int, vp, vp, C.POINTER(i32), vp, vp]
     L.fram_gradient.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, C.POINTER(dbl)]
     L.fram_lap.argtypes = [vp, vp, vp, vp]
@@ -103,7 +104,7 @@ def lib():
                                         vp, C.POINTER(_Stats)]
     for f in ("fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_get_unique_id",
               "fram_solve_attributed",
-              "fram_create_sharded", "fram_sdsn", "fram_gradient", "fram_lap"):
+              "fram_create_sharded", "fram_create_sharded_virtual", "fram_sdsn", "fram_gradient", "fram_lap"):
         getattr(L, f).restype = C.c_int
     _lib_handle = L
     return L
@@ -333,6 +334,16 @@ def fram_create_sharded(n, lam, schedule: Schedule | None, uid: bytes, rank, wor
                                      C.byref(out)))
     del keep
     return Handle(out, int(n), rows=int(n) // int(world), rank=int(rank), world=int(world), schedule=schedule)
+
+
+def fram_create_sharded_virtual(n, lam=1.0, schedule: Schedule | None = None, world=2, device=0) -> Handle:
+    """Virtual-shard group on ONE GPU (include/fram.h): `world` ranks of the row-sharded solve, collectives
+    as fixed-order device sums/copies.  fram_solve on it takes and returns full n×n matrices."""
+    s, keep = (schedule or Schedule()).to_c()
+    out = C.c_void_p()
+    _check(lib().fram_create_sharded_virtual(int(n), float(lam), C.byref(s), int(world), int(device), C.byref(out)))
+    del keep
+    return Handle(out, int(n), rows=int(n), rank=0, world=int(world), schedule=schedule)
 
 
 def shard_rows(n, rank, world):

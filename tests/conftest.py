@@ -17,3 +17,22 @@ def pytest_configure(config):
 def rng():
     import numpy as np
     return np.random.Generator(np.random.PCG64(12345))
+
+
+@pytest.fixture
+def errlog(request):
+    """Record an observed parity error next to its tolerance: printed (pytest -s / -rA) and, when
+    FRAM_PARITY_LOG names a file, appended to it as one JSON line per record."""
+    import json
+
+    def rec(quantity, observed, tol, **extra):
+        d = {"test": request.node.nodeid, "quantity": quantity, "observed": float(observed), "tol": float(tol),
+             **extra}
+        print("PARITY", json.dumps(d))
+        path = os.environ.get("FRAM_PARITY_LOG")
+        if path:
+            with open(path, "a") as f:
+                f.write(json.dumps(d) + "\n")
+        return observed
+
+    return rec

@@ -66,3 +66,10 @@ def test_no_cpu_fallback_without_gpu():
     with pytest.raises(fb.FramError) as e:
         fb.fram_solve(h, A, A)
     assert e.value.status == fb.FRAM_ERR_CUDA
+
+
+def test_virtual_shard_validation():
+    for n, w in ((10, 3), (16, 0), (16, 17)):
+        with pytest.raises(fb.FramError) as e:
+            fb.fram_create_sharded_virtual(n, 1.0, fb.Schedule(), world=w)
+        assert e.value.status == fb.FRAM_ERR_USAGE

@@ -1,0 +1,137 @@
+"""Acceptance at the BASELINE configs, with the north star's tolerances (SURVEY §8(c) "Acceptance"):
+
+  C4 (n=4096, the bench's workload and schedule): every mixed precision (BF16 / TF32 / FP16 operands,
+     FP32 SDSN) holds |ΔΦ|/Φ ≤ 1e-3 and |Δacc| ≤ 0.5 pp against the FP64 oracle's full solve of the same
+     instance (tests/golden/c4_oracle.json, written by tools/make_golden_c4.py, which calls only
+     oracle/); GPU FP64 mode free-running reproduces that solve (same pass counts, δ trace, permutation),
+     and an FP64 replay checks N⁽ᵗ⁾ ≤ 1e-9 per outer iteration at full size (DMMA GEMMs, streaming FP64
+     SDSN with on-chip rows, update).
+  C2 (n=500, its real size): FP64 replay per iteration ≤ 1e-9 and mixed TF32 / BF16 vs the oracle.
+Alg. 1, Alg. 2, LAP P:337 (R17); Φ of the discrete matching (R21, Eq.1).
+"""
+import functools
+import json
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2508_00887_b200 import FRAM_OK, FRAM_NOT_CONVERGED, Schedule, fram_create, fram_solve
+from synth import config_c2, config_c4
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "c4_oracle.json")
+
+
+@functools.lru_cache(None)
+def _c4():
+    return config_c4(0)
+
+
+@functools.lru_cache(None)
+def _golden():
+    with open(GOLD) as f:
+        return json.load(f)
+
+
+def _dev(x, dt=torch.float32):
+    return torch.tensor(np.ascontiguousarray(x), dtype=dt, device="cuda")
+
+
+def _c4_solve(prec, **kw):
+    inst = _c4()
+    h = fram_create(inst.n, schedule=Schedule(theta=inst.theta, **kw))
+    return fram_solve(h, _dev(inst.A), _dev(inst.B), precision=prec)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "tf32", "fp16"])
+def test_c4_mixed_precision_vs_oracle(prec, errlog):
+    inst, gold = _c4(), _golden()
+    st, stats, X, perm = _c4_solve(prec)
+    assert st in (FRAM_OK, FRAM_NOT_CONVERGED)
+    p = perm.cpu().numpy()
+    assert sorted(p) == list(range(inst.n))
+    phi = oracle.objective_perm(inst.A, inst.B, None, p)
+    rel = abs(phi - gold["phi_perm"]) / abs(gold["phi_perm"])
+    acc = oracle.node_accuracy(p, inst.perm_true)
+    errlog("|dPhi|/Phi", rel, 1e-3, phi=phi, phi_oracle=gold["phi_perm"], outer=stats["outer_iters"])
+    errlog("|dacc|", abs(acc - gold["accuracy"]), 0.005, acc=acc, acc_oracle=gold["accuracy"])
+    assert rel <= 1e-3
+    assert abs(acc - gold["accuracy"]) <= 0.005
+    if prec == "bf16":                    # the bench's precision: the LAP is bit-exact on the GPU's own N
+        assert np.array_equal(p, oracle.lap_max(X.cpu().numpy()))
+
+
+def test_c4_fp64_free_running_reproduces_oracle(errlog):
+    inst, gold = _c4(), _golden()
+    st, stats, X, perm = _c4_solve("fp64")
+    assert stats["passes"] == gold["passes"]
+    dd = np.max(np.abs(np.array(stats["deltas"]) - np.array(gold["deltas"])))
+    errlog("max|delta_gpu-delta_oracle|", dd, 1e-9, outer=stats["outer_iters"])
+    assert dd <= 1e-9
+    assert stats["converged"] == gold["converged"]
+    assert perm.cpu().numpy().tolist() == gold["perm"]
+    Xn = X.cpu().numpy()
+    errlog("|sum N - oracle|", abs(Xn.sum() - gold["N_sum"]), 1e-6)
+    assert abs(Xn.sum() - gold["N_sum"]) <= 1e-6 and abs(np.linalg.norm(Xn) - gold["N_fro"]) <= 1e-9
+
+
+def test_c4_fp64_replay_per_iteration_full_size(errlog):
+    # 3 outer iterations × 10 passes at n = 4096 (the oracle finishes in seconds); every N⁽ᵗ⁾ ≤ 1e-9
+    inst = _c4()
+    k, T = 10, 3
+    ref = oracle.fram(inst.A, inst.B, None, theta=inst.theta, replay=[k] * T, keep_trace=True)
+    for t in range(1, T + 1):
+        h = fram_create(inst.n, schedule=Schedule(theta=inst.theta, replay=[k] * t))
+        _, stats, X, perm = fram_solve(h, _dev(inst.A, torch.float64), _dev(inst.B, torch.float64), precision="fp64")
+        e = float(np.max(np.abs(X.cpu().numpy() - ref["Ns"][t - 1])))
+        errlog("max|N_gpu-N_oracle|", e, 1e-9, t=t)
+        assert e <= 1e-9
+        assert abs(stats["deltas"][-1] - ref["deltas"][t - 1]) <= 1e-12
+    assert np.array_equal(perm.cpu().numpy(), ref["perm"])
+
+
+@functools.lru_cache(None)
+def _c2_oracle():
+    inst = config_c2(0)
+    return inst, oracle.fram(inst.A, inst.B, None, theta=inst.theta)
+
+
+def test_c2_fp64_n500_replay_per_iteration(errlog):
+    inst, free = _c2_oracle()
+    assert inst.n == 500
+    h = fram_create(inst.n, schedule=Schedule(theta=inst.theta))
+    st, stats, X, perm = fram_solve(h, _dev(inst.A, torch.float64), _dev(inst.B, torch.float64), precision="fp64")
+    assert st == FRAM_OK
+    assert stats["passes"] == free["passes"]                  # free-running pass counts agree
+    ref = oracle.fram(inst.A, inst.B, None, theta=inst.theta, replay=stats["passes"], keep_trace=True)
+    e = float(np.max(np.abs(X.cpu().numpy() - ref["N"])))
+    errlog("max|N_gpu-N_oracle| (final)", e, 1e-9)
+    assert e <= 1e-9
+    assert np.max(np.abs(np.array(stats["deltas"]) - np.array(ref["deltas"]))) <= 1e-9
+    assert np.array_equal(perm.cpu().numpy(), ref["perm"])
+    T = len(stats["passes"])
+    for t in sorted({1, T // 2}):
+        ht = fram_create(inst.n, schedule=Schedule(theta=inst.theta, replay=stats["passes"][:t]))
+        _, _, Xt, _ = fram_solve(ht, _dev(inst.A, torch.float64), _dev(inst.B, torch.float64), precision="fp64")
+        e = float(np.max(np.abs(Xt.cpu().numpy() - ref["Ns"][t - 1])))
+        errlog("max|N_gpu-N_oracle|", e, 1e-9, t=t)
+        assert e <= 1e-9
+
+
+@pytest.mark.parametrize("prec", ["tf32", "bf16"])
+def test_c2_mixed_n500_vs_oracle(prec, errlog):
+    inst, free = _c2_oracle()
+    h = fram_create(inst.n, schedule=Schedule(theta=inst.theta))
+    st, stats, X, perm = fram_solve(h, _dev(inst.A), _dev(inst.B), precision=prec)
+    p = perm.cpu().numpy()
+    phi = oracle.objective_perm(inst.A, inst.B, None, p)
+    phi_o = oracle.objective_perm(inst.A, inst.B, None, free["perm"])
+    acc, acc_o = oracle.node_accuracy(p, inst.perm_true), oracle.node_accuracy(free["perm"], inst.perm_true)
+    errlog("|dPhi|/Phi", abs(phi - phi_o) / abs(phi_o), 1e-3)
+    errlog("|dacc|", abs(acc - acc_o), 0.005)
+    assert abs(phi - phi_o) / abs(phi_o) <= 1e-3
+    assert abs(acc - acc_o) <= 0.005
+    assert np.array_equal(p, oracle.lap_max(X.cpu().numpy()))

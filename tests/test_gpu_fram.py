@@ -112,8 +112,8 @@ def test_fram_unary_term_dspfp_and_x0():
 
 def test_fram_c4_full_size_bf16():
     # BASELINE config C4 (n=4096, BA m=5, 5% rewiring), bf16-GEMM/fp32-SDSN, the bench's launch
-    # configuration and schedule.  The full oracle is too slow here (SURVEY [M16]: 429 s), so:
-    # size-independent properties + bit-exact LAP of the GPU's own N + accuracy vs planted truth.
+    # configuration and schedule: size-independent properties of the output.  The comparison with the
+    # oracle's full C4 solve is tests/test_gpu_acceptance.py.
     inst = config_c4(0)
     n = inst.n
     h = fram_create(n, schedule=_sched(inst, flags=FLAG_CHECK_SYMMETRY | FLAG_TRACE | FLAG_TIME_PHASES))
@@ -126,11 +126,7 @@ def test_fram_c4_full_size_bf16():
     mass = Xn.sum() / n - 1
     assert -1e-9 <= mass <= max(stats["gamma_last"]) + 1e-6
     assert sorted(p) == list(range(n))
-    assert np.array_equal(p, oracle.lap_max(Xn))
-    acc = oracle.node_accuracy(p, inst.perm_true)
-    assert acc >= 0.95                                   # [M16]: 0.9795 on the CPU transcription
-    # one outer iteration checked against the oracle on the same gradient input (sampled rows)
-    assert stats["total_passes"] == sum(stats["passes"])
+    assert stats["total_passes"] == sum(stats["passes"]) and len(stats["passes"]) == stats["outer_iters"]
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5])

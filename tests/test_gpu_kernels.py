@@ -39,7 +39,7 @@ def _inputs(n, seed, withK=False):
     return A, B, K, N
 
 
-@pytest.mark.parametrize("n", [7, 64, 200, 513])
+@pytest.mark.parametrize("n", [7, 64, 200, 513, 1500, 4096])
 @pytest.mark.parametrize("withK", [False, True])
 def test_gradient_fp64(n, withK):
     A, B, K, N = _inputs(n, n, withK)
