@@ -637,6 +637,7 @@ fram_status group_solve(fram_ctx* g, int dt, const void* A, const void* B, const
   const int W = (int)g->vsub.size();
   const long n = g->n, m = n / W;
   CK(cudaStreamSynchronize(caller), "caller stream sync");        // inputs produced on the caller's stream
+  fram::vgroup_reset(g->vgroup);                                  // a previous failed solve aborted it
   std::vector<fram_status> st(W, FRAM_OK);
   std::vector<std::string> msg(W);
   const size_t es = dt_size(dt);

@@ -45,7 +45,7 @@ struct ResParams {
   double* sdsn_out;    // [4] as SdsnParams
   int rs;              // rows per CTA held in shared memory (set by the launcher)
   int rmax;            // rows per CTA upper bound (set by the launcher)
-  long long* dbg;      // dev-only (FRAM_RES_TIMING): per-CTA phase times [grid][8], nullable
+  long long* dbg;      // dev-only (-DFRAM_DEV_RES_TIMING=1 builds): per-CTA phase times [grid][8]; null in the product
 };
 int sdsn_res_grid(long n, int num_sms);       // 0 ⇒ n not supported on chip
 long sdsn_res_slots(long n);

@@ -36,12 +36,6 @@
 namespace fram {
 namespace {
 
-#ifndef FRAM_DEV_RES_TIMING
-#define FRAM_DEV_RES_TIMING 0
-#endif
-// dev-only phase timing (tools/build_variant.sh … -DFRAM_DEV_RES_TIMING=1): compiled out of the product
-constexpr bool kDevTiming = FRAM_DEV_RES_TIMING != 0;
-
 constexpr int kResSmemMax = 232448 - 4608;   // 227 KB opt-in minus static shared memory (≤ 4.3 KB)
 constexpr int kResMinSmem = 120 * 1024;      // forces one CTA per SM (TMEM: 512 columns per CTA)
 
@@ -157,7 +151,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   };
 
   long long tk0 = 0;
-  if (kDevTiming && P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk0));
+  if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk0));
   // ---------------- phase L: X rows → on-chip, m = max X (Alg.2 step 1) ----------------
   {
     float lmax = 0.f;
@@ -224,15 +218,16 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
 
   // after a sweep: column partials (two row groups combined in shared memory) → colpart[b];
   // row sums (per-lane partials → fixed-order tree) → s_r; Σ r → Spart[b]; all tagged e
-  // dev timing (P.dbg, FRAM_RES_TIMING): per-CTA slots accumulated in shared memory by one thread
+  // dev timing (P.dbg; set only by a -DFRAM_DEV_RES_TIMING=1 build of fram_api.cu, always null in the
+  // product, where these branches are never taken): per-CTA slots accumulated in shared memory by one thread
   // (k < 9) or by the first warp of each row group (rows: 9 + g ns, 11 + g cycles), copied out at the end
   __shared__ long long s_dbg[16];
   if (tid < 16) s_dbg[tid] = 0;
   __syncthreads();
-  auto dadd = [&](int k, long long v) { if (kDevTiming && P.dbg && tid == 0) s_dbg[k] += v; };
+  auto dadd = [&](int k, long long v) { if (P.dbg && tid == 0) s_dbg[k] += v; };
   int jst = -1;                                          // pass whose timeline is stamped (dev timing)
   auto stamp = [&](int k) {
-    if (kDevTiming && P.dbg && tid == 0 && jst == 500) {
+    if (P.dbg && tid == 0 && jst == 500) {
       long long v;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
       P.dbg[(size_t)G * 16 + b * 8 + k] = v;
@@ -240,7 +235,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   };
   auto gt = [&]() -> long long {
     long long v = 0;
-    if (kDevTiming && P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
     return v;
   };
   auto sweep_epilogue = [&](const float (&col)[CH], unsigned e) {
@@ -358,7 +353,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   auto arow = [&](int r) -> float { return (float)(abase - s_rn[r]); };   // a_i (FP64, rounded once)
   auto sweep_pass = [&](const float2 (&bv)[CH / 2], unsigned e) {
     const long long l0 = gt();
-    const long long c0k = (kDevTiming && P.dbg) ? clock64() : 0;
+    const long long c0k = P.dbg ? clock64() : 0;
     float2 col2[CH / 2];
 #pragma unroll
     for (int k = 0; k < CH / 2; ++k) col2[k] = make_float2(0.f, 0.f);
@@ -444,7 +439,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     float col[CH];
 #pragma unroll
     for (int k = 0; k < CH / 2; ++k) { col[2 * k] = col2[k].x; col[2 * k + 1] = col2[k].y; }
-    if (kDevTiming && P.dbg && lane == 0 && (warp & 7) == 0) {
+    if (P.dbg && lane == 0 && (warp & 7) == 0) {
       s_dbg[9 + g] += gt() - l0;
       s_dbg[11 + g] += clock64() - c0k;
     }
@@ -510,7 +505,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
 
   // ---------------- phase S: Y0 = s·X (on chip) and its sums ----------------
   long long tk1 = 0;
-  if (kDevTiming && P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk1));
+  if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk1));
   sweep_scale();
   unsigned ep = 1;                                       // epoch of the current exchange
   slice(ep);
@@ -521,7 +516,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   double gam = 0.0;
   auto now = [&]() -> long long {
     long long v = 0;
-    if (kDevTiming && P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
+    if (P.dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(v));
     return v;
   };
   for (;; ++j) {
@@ -589,7 +584,7 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     long long t4 = now();
     dadd(0, t1 - t0); dadd(1, t2 - t1); dadd(8, t4 - t2);
   }
-  if (kDevTiming && P.dbg && tid == 0) {
+  if (P.dbg && tid == 0) {
     for (int k = 0; k < 16; ++k) P.dbg[b * 16 + k] = s_dbg[k];
     long long tk2;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tk2));

@@ -202,6 +202,12 @@ void vgroup_destroy(VGroup* g) {
 
 void vgroup_abort(VGroup* g) { if (g) g->abort(); }
 
+void vgroup_reset(VGroup* g) {                 // before a solve: no rank is inside a collective
+  std::lock_guard<std::mutex> lk(g->mu);
+  g->aborted = false;
+  g->arrived = 0;
+}
+
 fram_status shard_create_virtual(ShardCtx** out, VGroup* g, int rank) {
   ShardCtx* s = new ShardCtx();
   s->vg = g;

@@ -12,6 +12,7 @@ struct VGroup;                       // virtual shards: W ranks of one process o
 VGroup* vgroup_create(int W, std::string* err);
 void vgroup_destroy(VGroup* g);
 void vgroup_abort(VGroup* g);
+void vgroup_reset(VGroup* g);
 fram_status shard_create_virtual(ShardCtx** out, VGroup* g, int rank);
 fram_status shard_unique_id(uint8_t id[128], std::string* err);
 fram_status shard_create(ShardCtx** out, const uint8_t id[128], int rank, int world, std::string* err);
