@@ -935,6 +935,11 @@ fram_status fram_lap(fram_handle h, const double* Nin, int32_t* perm_out, void* 
     if (hbad) return fail(FRAM_ERR_DATA, "N must be finite");
   }
   CK(fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
+  int lap_err = 0;
+  CK(cudaMemcpyAsync(&lap_err, static_cast<char*>(h->lapw.p) + fram::lap_err_offset(n), sizeof(int),
+                     cudaMemcpyDeviceToHost, st), "lap status");
+  CK(cudaStreamSynchronize(st), "sync");
+  if (lap_err) return fail(FRAM_ERR_DATA, "LAP found no finite candidate column (non-finite N)");
   CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
   CK(cudaStreamSynchronize(st), "sync");
   return FRAM_OK;

@@ -125,6 +125,7 @@ cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long ro
 cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* work,
                        cudaStream_t st);
 size_t lap_work_bytes(long n);
+size_t lap_err_offset(long n);     // byte offset of the LAP kernels' error word in the workspace (int, 0 = ok)
 
 // ---- misc ---------------------------------------------------------------------------------------
 cudaError_t launch_pad_convert(double* dst, long ldd, long drows, long dcols, const void* src, int dt, long lds,

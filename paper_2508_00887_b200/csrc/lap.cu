@@ -47,7 +47,7 @@ __device__ __forceinline__ void warp_argmin(uint64_t& key, int& j) {
 
 template <int THREADS, int CPT, bool SMEM>
 __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restrict__ N, int n, long ld,
-                                                         int32_t* perm, void* gwork) {
+                                                         int32_t* perm, void* gwork, int* err) {
   constexpr int WARPS = THREADS / 32;
   extern __shared__ __align__(16) unsigned char dsm[];
   __shared__ uint64_t s_k[2][WARPS];                  // per-warp argmin candidates, double-buffered
@@ -139,6 +139,10 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
       warp_argmin(dkey, j1);
       const double delta = unkey(dkey);
       par ^= 1;
+      if (j1 > n) {                                   // no finite candidate (non-finite N): give up cleanly
+        if (tid == 0) *err = 1;
+        return;                                       // j1 is the same in every thread
+      }
       const int i0n = p[j1];                          // p is not modified during a search
       if (i0n != 0) load_row(i0n);                    // next row's loads overlap the updates below
       // potentials: used columns (u[p[j]] += δ, v[j] −= δ), virtual column 0 (u[i] += δ), free minv −= δ
@@ -190,9 +194,19 @@ __global__ void __launch_bounds__(THREADS, 1) lap_kernel(const double* __restric
 // trow[], known to all from the records, by the same FP64 adds in the same order) and pw[j] = way[j]
 // of the tree columns (final once a column is used, sent in its record).  way[] of the free columns
 // stays local (wl[]).  All float operations equal lap_kernel's, so the result is bit-exact with R17.
+//
+// Deferred row potentials.  Within one search u is read only for the row entering the tree (u[i0]),
+// which the search has not touched yet; the root and the tree rows are never read again before the
+// search ends.  So instead of adding δ_s to every tree row at every step (O(tree) shared-memory
+// read-modify-writes per step, up to ~13 per thread in the longest C4 searches), step s only records
+// δ_s, and at the search end every tree row replays ITS suffix of the δ sequence, u += δ_e, δ_{e+1}, …,
+// δ_{S−1} (e = the step after it entered; the root: all steps) — the same FP64 adds in the same order,
+// so u is bit-identical to the step-by-step update.  A thread replays 4 rows at once (independent
+// add chains).  The δ history lives in global memory (one store by one thread per step).
 template <int CS, int CPT, int THREADS, bool UG>
 __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* __restrict__ N, int n, long ld,
-                                                                 int32_t* perm, double* ug) {
+                                                                 int32_t* perm, double* ug, double* dhist,
+                                                                 int* err) {
   constexpr int WARPS = THREADS / 32, CH = THREADS * CPT, NREC = CS * WARPS;
   constexpr uint32_t REC_BYTES = NREC * 16;
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -203,6 +217,7 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
   // fit) in this CTA's private copy in global memory — u is read once per step (u[i0], issued with
   // the row loads) and updated for the tree rows by the same thread every step
   double* u = UG ? ug + (size_t)blockIdx.x * m : reinterpret_cast<double*>(dsm);
+  double* dh = dhist + (size_t)blockIdx.x * m;          // δ of each step of the current search
   int* p = UG ? reinterpret_cast<int*>(dsm) : reinterpret_cast<int*>(u + m);   // [m] replicated matching
   int* pw = p + m;                                    // [m] way of tree columns (replicated)
   int* trow = pw + m;                                 // [m] rows that entered the tree (this search)
@@ -328,7 +343,11 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
       wy1 = __shfl_sync(0xffffffffu, wy1, __ffs(who) - 1);
       const double delta = unkey(dkey);
       ++step;
-      if (tid == 0) pw[j1] = wy1;                     // way of the column entering the tree (final)
+      if (j1 > n) {                                   // no finite candidate (non-finite N): give up cleanly
+        if (c == 0 && tid == 0) *err = 1;
+        return;                                       // every CTA reduced the same records: all return
+      }
+      if (tid == 0) { pw[j1] = wy1; dh[ntree] = delta; }   // way of the entering column (final); δ_s, s = ntree
       const int i0n = p[j1];
       if (i0n != 0) load_row(i0n);
       const uint32_t usd = inr & ~fr;
@@ -337,15 +356,35 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
         if ((usd >> k) & 1u) v[k] = __dsub_rn(v[k], delta);
         minv[k] = __dsub_rn(minv[k], delta);
       }
-      // each tree row's u is updated by the same thread at every step; no tree row's u is read during
-      // the search (u[i0] of the row entering the tree is not updated in the step that selects it)
-      for (int t = tid; t < ntree; t += THREADS) u[trow[t]] = __dadd_rn(u[trow[t]], delta);
-      if (tid == 0) u[i] = __dadd_rn(u[i], delta);
       j0 = j1;
       i0 = i0n;
       if (i0 == 0) break;
     }
-    __syncthreads();                                  // pw[], p[], u[] final for this search
+    __syncthreads();                                  // pw[], p[], trow[] and the δ history final
+    {   // replay: row q = 0 is the root (δ_0 … δ_{S−1}), row q ≥ 1 is trow[q−1] (δ_q … δ_{S−1}), S = ntree + 1
+      const int S = ntree + 1;
+      for (int q0 = tid; q0 <= ntree; q0 += 4 * THREADS) {
+        double uu[4];
+        int rr[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int q = q0 + k * THREADS;
+          rr[k] = q <= ntree ? (q == 0 ? i : trow[q - 1]) : 0;
+          uu[k] = q <= ntree ? u[rr[k]] : 0.0;
+        }
+#pragma unroll 4
+        for (int s = q0; s < S; ++s) {
+          const double d = dh[s];
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (s >= q0 + k * THREADS) uu[k] = __dadd_rn(uu[k], d);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (q0 + k * THREADS <= ntree) u[rr[k]] = uu[k];
+      }
+    }
+    __syncthreads();                                  // u final for this search
     if (tid == 0) {                                   // augment along way[] (every CTA, same walk)
       int jj = j0;
       do {
@@ -363,6 +402,10 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
 
 template <int CS, int CPT, int THREADS = 512, bool UG = false>
 cudaError_t launch_cluster_t(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
+  // work: [UG: CS × (n+1) u copies] [CS × (n+1) δ histories] [error word]
+  double* ug = reinterpret_cast<double*>(work);
+  double* dhist = ug + (UG ? (size_t)CS * (n + 1) : 0);
+  int* err = reinterpret_cast<int*>(static_cast<char*>(work) + lap_err_offset(n));
   auto fn = lap_cluster_kernel<CS, CPT, THREADS, UG>;
   const size_t m = (size_t)n + 1;
   const size_t bytes = m * ((UG ? 0 : sizeof(double)) + 3 * sizeof(int)) + (size_t)THREADS * CPT * sizeof(int) + 64;
@@ -381,34 +424,41 @@ cudaError_t launch_cluster_t(const double* N, long n, long ld, int32_t* perm, vo
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, fn, N, (int)n, ld, perm, reinterpret_cast<double*>(work));
+  return cudaLaunchKernelEx(&cfg, fn, N, (int)n, ld, perm, ug, dhist, err);
 }
 
 template <int THREADS, int CPT>
 cudaError_t launch_t(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
-  const size_t bytes = lap_work_bytes(n);
+  const size_t bytes = (size_t)(n + 1) * (sizeof(double) + 2 * sizeof(int)) + 64;   // u, p, way
+  int* err = reinterpret_cast<int*>(static_cast<char*>(work) + lap_err_offset(n));
   if (bytes <= 200 * 1024) {
     auto fn = lap_kernel<THREADS, CPT, true>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    fn<<<1, THREADS, bytes, st>>>(N, (int)n, ld, perm, work);
+    fn<<<1, THREADS, bytes, st>>>(N, (int)n, ld, perm, work, err);
   } else {
-    lap_kernel<THREADS, CPT, false><<<1, THREADS, 0, st>>>(N, (int)n, ld, perm, work);
+    lap_kernel<THREADS, CPT, false><<<1, THREADS, 0, st>>>(N, (int)n, ld, perm, work, err);
   }
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// single-CTA kernel: u, p, way in global memory; cluster kernel with u in global memory (n > 8192):
-// one u copy per CTA of the cluster (≤ 16)
+// single-CTA kernel: u, p, way in global memory; cluster kernel: per CTA of the cluster (≤ 16) a δ
+// history and, for n > 8192, a u copy, then an error word
 size_t lap_work_bytes(long n) {
   const size_t single = (size_t)(n + 1) * (sizeof(double) + 2 * sizeof(int)) + 64;
-  const size_t cl = n > 8192 ? (size_t)(n + 1) * sizeof(double) * 16 : 0;
+  const size_t cl = (size_t)(n + 1) * sizeof(double) * 16 * (n > 8192 ? 2 : 1) + 64;
   return single > cl ? single : cl;
 }
 
+size_t lap_err_offset(long n) {            // byte offset of the error word (past every kernel's arrays)
+  return lap_work_bytes(n) - 8;
+}
+
 cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* work, cudaStream_t st) {
+  cudaError_t e0 = cudaMemsetAsync(static_cast<char*>(work) + lap_err_offset(n), 0, sizeof(int), st);
+  if (e0 != cudaSuccess) return e0;
   if (n <= 256) return launch_t<256, 1>(N, n, ld, perm, work, st);
   if (n <= 512) return launch_t<512, 1>(N, n, ld, perm, work, st);
   if (n <= 1024) return launch_t<512, 2>(N, n, ld, perm, work, st);

@@ -9,7 +9,7 @@ python -c "from paper_2508_00887_b200 import build as b; b.build()" >/dev/null
 B=paper_2508_00887_b200/build
 mkdir -p /tmp/fram_variant tools/ab
 base=$(basename $src .cu)
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -Iinclude \
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-fvisibility=hidden -Iinclude -Ipaper_2508_00887_b200/csrc \
   --expt-relaxed-constexpr "$@" -c paper_2508_00887_b200/csrc/$src -o /tmp/fram_variant/$base.o
 objs=""
 for o in $B/*.o; do
