@@ -431,16 +431,8 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       }
     };
     if (R > RT) {
-#if defined(K4R_SPLIT_SHIFT) && K4R_SPLIT_SHIFT > 0       // dev A/B: group 1 also takes the last TMEM rows
-      if (g == 0) rows_tmem(0, RT - K4R_SPLIT_SHIFT, 1);
-      else { rows_tmem(RT - K4R_SPLIT_SHIFT, RT, 1); rows_smem(RT, R); }
-#elif defined(K4R_SPLIT_SHIFT) && K4R_SPLIT_SHIFT < 0     // dev A/B: group 0 also takes the first SMEM rows
-      if (g == 0) { rows_tmem(0, RT, 1); rows_smem(RT, min(R, RT - K4R_SPLIT_SHIFT)); }
-      else rows_smem(min(R, RT - K4R_SPLIT_SHIFT), R);
-#else
       if (g == 0) rows_tmem(0, RT, 1);
       else rows_smem(RT, R);
-#endif
     } else {
       rows_tmem(g, R, 2);
     }
