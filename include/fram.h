@@ -95,8 +95,7 @@ typedef struct {
   int32_t sdsn_capped_calls; /* SDSN calls that stopped on sdsn_max                               */
   int32_t sdsn_kernel;       /* SDSN kernel used: 1 streaming (K4), 2 on-chip resident (K4r),
                                 3 row-sharded per-pass kernels + NCCL (K4s), 4 one thread-block
-                                cluster with a DSMEM all-reduce (K4c, small n), 5 on-chip with the
-                                column all-reduce pipelined behind half-sweeps (K4p, 1024 < n ≤ 4096) */
+                                cluster with a DSMEM all-reduce (K4c, small n)                      */
   int64_t total_passes;      /* Σ_t passes_t                                                     */
   int32_t* passes_per_iter;  /* [max_outer] SDSN passes of outer iteration t                     */
   double*  delta_trace;      /* [max_outer] δ_t                                          */

@@ -179,9 +179,8 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
   CK(h->colpart.ensure((size_t)G * ld * (f64 ? 8 : 4)), "alloc colpart");
   CK(h->Spart.ensure(2 * (size_t)std::max(G, h->num_sms) * 8), "alloc Spart");   // [2][G] tagged (K4)
   CK(h->Mpart.ensure((size_t)std::max(G, h->num_sms) * 8), "alloc Mpart");
-  if (!f64 && (fram::sdsn_res_grid(n, h->num_sms) > 0 || fram::sdsn_pipe_grid(n, h->num_sms) > 0)) {
-    const size_t w = std::max(fram::sdsn_res_xchg_words(n, h->num_sms), fram::sdsn_pipe_xchg_words(n, h->num_sms));
-    CK(h->rcolpart.ensure(w * 8), "alloc on-chip exchange");
+  if (!f64 && fram::sdsn_res_grid(n, h->num_sms) > 0) {
+    CK(h->rcolpart.ensure(fram::sdsn_res_xchg_words(n, h->num_sms) * 8), "alloc resident exchange");
   }
   CK(h->cvec.ensure((size_t)ld * 8), "alloc cvec");
   CK(h->bar.ensure(64), "alloc bar");
@@ -268,15 +267,8 @@ fram_status gradient(fram_ctx* h, int op, bool haveK, cudaStream_t st) {
 #ifndef FRAM_DEV_RES_TIMING
 #define FRAM_DEV_RES_TIMING 0
 #endif
-#ifndef FRAM_DEV_PIPE
-#define FRAM_DEV_PIPE 0
-#endif
-// 5 = K4p (FP32 on chip with the column all-reduce pipelined behind half-sweeps, 1024 < n ≤ 4096):
-// correct but measured slower than K4r (8.5 vs 6.6 µs per pass at n = 4096), so only a
-// -DFRAM_DEV_PIPE=1 dev build selects it
 int sdsn_kind(const fram_ctx* h, bool f64) {
   if (FRAM_DEV_FORCE_STREAM) return 1;
-  if (FRAM_DEV_PIPE && !f64 && fram::sdsn_pipe_grid(h->n, h->num_sms) > 0) return 5;
   // K4c where it measured fastest (tools/sdsn_small_timing.py): FP64 up to its size limit (vs K4),
   // FP32 only for n ≤ 160 (with the mbarrier hand-off K4c and K4r tie at n = 256, K4r is faster above)
   if (!FRAM_DEV_NOCLUSTER && !h->no_cluster && fram::sdsn_cluster_supported(h->n, f64) && (f64 || h->n <= 160))
@@ -313,24 +305,6 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
       CK(ce, "sdsn (cluster) launch");
     cudaGetLastError();
     h->no_cluster = true;
-  }
-  if (sdsn_kind(h, f64) == 5) {
-    fram::ResParams r{};
-    r.Y = h->Y.as<float>();
-    r.n = h->n;
-    r.ld = h->ld;
-    r.theta = h->sched.theta;
-    r.gamma_th = h->sched.gamma_th;
-    r.sdsn_max = h->sched.sdsn_max;
-    r.sdsn_fixed = fixed;
-    r.scale = (h->sched.flags & FRAM_FLAG_NO_THETA_SCALE) ? 0 : 1;
-    r.xchg = h->rcolpart.as<uint64_t>();
-    r.passes_out = reinterpret_cast<int*>(scal + 8);
-    r.gamma_hist = h->ghist.as<double>();
-    r.sdsn_out = scal;
-    CK(fram::launch_sdsn_pipe(r, st, h->num_sms), "sdsn (pipelined on-chip) launch");
-    h->launches += 2;   // exchange memsets + kernel
-    return FRAM_OK;
   }
   if (use_resident(h, f64)) {
     fram::ResParams r{};

@@ -51,11 +51,6 @@ int sdsn_res_grid(long n, int num_sms);       // 0 ⇒ n not supported on chip
 long sdsn_res_slots(long n);
 size_t sdsn_res_xchg_words(long n, int num_sms);   // size of ResParams::xchg
 cudaError_t launch_sdsn_resident(const ResParams& p, cudaStream_t st, int num_sms);
-// K4p (sdsn_pipe.cu): the on-chip kernel with the column all-reduce pipelined behind half-sweeps
-// (1024 < n ≤ 4096); same ResParams, its own exchange size
-int sdsn_pipe_grid(long n, int num_sms);        // 0 ⇒ n not supported
-size_t sdsn_pipe_xchg_words(long n, int num_sms);
-cudaError_t launch_sdsn_pipe(const ResParams& p, cudaStream_t st, int num_sms);
 
 // ---- K4s: SDSN on a row block for the sharded solve (per-pass kernels + host NCCL all-reduce) ----
 struct ShardSdsnState {
