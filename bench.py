@@ -51,10 +51,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-extra-precisions", action="store_true",
                    help="skip the TF32 (the paper's step-5 precision) and FP64 C4 solves reported beside the main line")
-    p.add_argument("--workload", default="c4", choices=["c4", "c3", "c5"],
+    p.add_argument("--workload", default="c4", choices=["c4", "c3", "c5", "ubc"],
                    help="c4: the metric's config (n=4096, replicas across ranks); c3: 4096 keypoint instances "
                         "(n=64) split across the ranks, one CTA per instance; c5: n=16384 row-sharded across "
-                        "the ranks (NCCL).  c3/c5 are not part of the default run")
+                        "the ranks (NCCL); ubc: NEXT-2, the paper's ubc(2000) regime (n=2000 fully connected "
+                        "keypoint graphs with 128-d features, theta=2), mixed vs FP64.  c3/c5/ubc are not part of "
+                        "the default run")
     p.add_argument("--max-outer", type=int, default=None, help="c5: cap on outer iterations per solve (bounded runs)")
     return p.parse_args()
 
@@ -598,7 +600,7 @@ def run_c3(args):
         line = {"metric": "FRAM batched instances/s (C3)", "value": total * args.steps / (tot_ms / 1e3),
                 "unit": "instances/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": tot_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-                "vs_baseline": None, "dtype": f"{args.precision}-gemm/f32-sdsn/f64-update",
+                "vs_baseline": None, "dtype": dtype_label(args.precision),
                 "data": "synthetic (seeded C3 keypoint generator)",
                 "config": {"workload": "C3: 4096 x n=64 keypoint graphs, unary K, theta=2", "batch": total,
                            "precision": args.precision, "parallelism": f"instances split over {world} rank(s)"},
@@ -610,6 +612,73 @@ def run_c3(args):
     return 0
 
 
+def run_ubc(args):
+    """NEXT-2: the attributed, fully connected keypoint-graph regime of the paper's mixed-precision
+    headline, ubc(2000) (graphs from images P:1047), on the synthetic stand-in synth.config_ubc
+    (UBC images are not available).  One step = fram_solve_attributed (K = F F̃ᵀ on the device, Alg. 1) at
+    n = 2000, θ = 2; the same solve in FP64 mode is timed beside it, giving the analogue of the paper's
+    12.7× mixed-vs-GPU-FP64 ratio.  Quality: matching error and Φ(M) on the device (fram_evaluate)."""
+    import numpy as np
+    import torch
+
+    import paper_2508_00887_b200 as fb
+    from synth import config_ubc
+
+    rank, world, local = dist_env()
+    if rank != 0:
+        return 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    n = 2000 if args.n == 4096 else args.n
+    inst = config_ubc(0, n=n)
+    A = torch.tensor(inst.A, dtype=torch.float64, device=dev)
+    B = torch.tensor(inst.B, dtype=torch.float64, device=dev)
+    F = torch.tensor(inst.meta["F"], dtype=torch.float64, device=dev)
+    Ft = torch.tensor(inst.meta["Ft"], dtype=torch.float64, device=dev)
+    sch = fb.Schedule(theta=inst.theta, alpha=SCHEDULE["alpha"], gamma_th=SCHEDULE["gamma_th"],
+                      delta_th=SCHEDULE["delta_th"], max_outer=SCHEDULE["max_outer"], sdsn_max=SCHEDULE["sdsn_max"],
+                      flags=fb.FLAG_TRACE | fb.FLAG_CHECK_SYMMETRY | fb.FLAG_TIME_PHASES)
+    h = fb.fram_create(n, lam=SCHEDULE["lam"], schedule=sch, device=local)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    res = {}
+    sampler = ClockSampler(local)
+    for prec in (args.precision, "fp64"):
+        for _ in range(args.warmup):
+            fb.fram_solve_attributed(h, A, B, F, Ft, precision=prec)
+        torch.cuda.synchronize()
+        if prec == args.precision:
+            sampler.start()
+        ms, its, stats = [], 0, None
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _, stats, X, perm = fb.fram_solve_attributed(h, A, B, F, Ft, precision=prec)
+            b.record()
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+            its += stats["outer_iters"]
+        clocks = sampler.stop() if prec == args.precision else None
+        p = perm.cpu().numpy()
+        ev = fb.fram_evaluate(h, A, B, torch.tensor(p, dtype=torch.int32, device=dev), F, Ft)
+        res[prec] = {"time_to_solution_ms": statistics.median(ms), "iters_per_s": its / (sum(ms) / 1e3),
+                     "outer_iters_per_solve": its / args.steps, "mean_passes_per_iter": stats["total_passes"] /
+                     max(1, stats["outer_iters"]), "accuracy": float((p == inst.perm_true).mean()),
+                     "matching_error": ev["matching_error"], "phi": ev["phi"], "ms_sdsn": stats["ms_sdsn"],
+                     "ms_gemm": stats["ms_gemm"], "ms_lap": stats["ms_lap"], "clocks": clocks}
+    main = res[args.precision]
+    line = {"metric": "ubc(2000)-regime time to solution (NEXT-2)", "value": main["time_to_solution_ms"], "unit": "ms",
+            "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
+            "dtype": dtype_label(args.precision), "data": "synthetic (synth.config_ubc: UBC ubc(2000) stand-in)",
+            "config": {"workload": "UBC stand-in: n=2000 fully connected Euclidean-distance graphs, d=128 features, "
+                                   "theta=2, lambda=1", "n": n, "precision": args.precision, "schedule": SCHEDULE},
+            "mixed": main, "fp64": res["fp64"],
+            "fp64_over_mixed_time_to_solution": res["fp64"]["time_to_solution_ms"] / main["time_to_solution_ms"],
+            "paper_context": "12.7x mixed over GPU-FP64 on an RTX 4080 SUPER (P:551), whose FP64 rate is 1/64 of FP32"}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -618,6 +687,8 @@ def main():
         return run_c5(args)
     if args.workload == "c3":
         return run_c3(args)
+    if args.workload == "ubc":
+        return run_ubc(args)
     return run_ours(args)
 
 

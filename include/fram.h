@@ -183,6 +183,17 @@ FRAM_API fram_status fram_create_sharded(int64_t n, double lambda, const fram_sc
 FRAM_API fram_status fram_create_sharded_virtual(int64_t n, double lambda, const fram_schedule* s, int world,
                                                 int device, fram_handle* out);
 
+/* Evaluation of a discrete matching (not on the solve's path): M[i, perm[i]] = 1 for the handle's n.
+ *  out[0] = ½‖A − MÃMᵀ‖_F + ‖F − MF̃‖_F   — the paper's matching error (with F = NULL only
+ *           the edge term, as P:380 prescribes for graphs without node attributes)
+ *  out[1] = ½‖A − MÃMᵀ‖_F                 out[2] = ‖F − MF̃‖_F
+ *  out[3] = Φ(M) = ½⟨MᵀAM, Ã⟩ + λ⟨MᵀF, F̃⟩  (Eq.(1), λ of the handle; K = F F̃ᵀ)
+ *  A, B: n×n, F, Ft: n×d (NULL ⇒ no feature term), all of storage `dt`, device or host; perm: int32[n]
+ *  (device or host); out: host double[4].  Sums in FP64 in a fixed order (deterministic).  A perm
+ *  entry outside [0, n) → FRAM_ERR_DATA. */
+FRAM_API fram_status fram_evaluate(fram_handle h, fram_dtype dt, const void* A, const void* B, const void* F,
+                                   const void* Ft, int64_t d, const int32_t* perm, void* stream, double out[4]);
+
 /* ---- test entry points (parity harness) ----------------------------------------------------
  * fram_sdsn: one SDSN call (Alg.2) on a nonnegative n×n X.  p = FRAM_PREC_FP64: X and
  *   D_out are FP64; any other p: FP32.  Uses the handle's θ, γ_th, sdsn_max, sdsn_fixed and the

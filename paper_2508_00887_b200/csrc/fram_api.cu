@@ -70,6 +70,7 @@ struct fram_ctx {
   DevBuf shUT, shUblk, shRsum, shSend, shRecv, shState, shNfull, shColpart, shScan;   // sharded solve
   DevBuf atA, atB, atK, atF, atFt, atPerm;                                           // attributed solve   // on-chip-resident SDSN (K4r)
   DevBuf stA, stB, stK, stX0, stX;
+  DevBuf evPart, evOut, evPerm;                                                        // evaluation (K9)
   DevBuf scan;
   double* hscal = nullptr;          // pinned readback
   cudaEvent_t ev[8] = {};
@@ -716,7 +717,7 @@ void fram_destroy(fram_handle h) {
                     &h->cvec, &h->bar, &h->scal, &h->ghist, &h->upd, &h->lapw, &h->permd, &h->stA, &h->stB,
                     &h->stK, &h->stX0, &h->stX, &h->scan, &h->rcolpart, &h->rbvec, &h->rflags, &h->rdbg, &h->shUT, &h->shUblk, &h->shRsum,
                     &h->shSend, &h->shRecv, &h->shState, &h->shNfull, &h->shColpart, &h->shScan, &h->atA,
-                    &h->atB, &h->atK, &h->atF, &h->atFt, &h->atPerm};
+                    &h->atB, &h->atK, &h->atF, &h->atFt, &h->atPerm, &h->evPart, &h->evOut, &h->evPerm};
   for (DevBuf* b : bufs) b->release();
   if (h->hscal) cudaFreeHost(h->hscal);
   for (auto& e : h->ev)
@@ -1048,6 +1049,45 @@ fram_status fram_create_sharded_virtual(int64_t n, double lambda, const fram_sch
     *out = nullptr;
   }
   return st;
+}
+
+fram_status fram_evaluate(fram_handle h, fram_dtype dt, const void* A, const void* B, const void* F, const void* Ft,
+                          int64_t d, const int32_t* perm, void* stream, double out[4]) {
+  fram_status s0 = common_checks(h, (int)dt, FRAM_PREC_FP64);
+  if (s0 != FRAM_OK) return s0;
+  if (!h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a virtual-shard group");
+  if (!A || !B || !perm || !out) return fail(FRAM_ERR_USAGE, "A, B, perm and out are required");
+  if ((F == nullptr) != (Ft == nullptr) || (F && d < 1)) return fail(FRAM_ERR_USAGE, "F and Ft go together, d >= 1");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const long n = h->n;
+  const size_t es = dt_size((int)dt);
+  fram_status rs;
+  const void *dA, *dB, *dF = nullptr, *dFt = nullptr, *dP;
+  if ((rs = stage_in(h, h->stA, A, (size_t)n * n * es, st, &dA)) != FRAM_OK) return rs;
+  if ((rs = stage_in(h, h->stB, B, (size_t)n * n * es, st, &dB)) != FRAM_OK) return rs;
+  if (F) {
+    if ((rs = stage_in(h, h->atF, F, (size_t)n * d * es, st, &dF)) != FRAM_OK) return rs;
+    if ((rs = stage_in(h, h->atFt, Ft, (size_t)n * d * es, st, &dFt)) != FRAM_OK) return rs;
+  }
+  if ((rs = stage_in(h, h->evPerm, perm, (size_t)n * 4, st, &dP)) != FRAM_OK) return rs;
+  CK(h->evPart.ensure((size_t)n * 4 * 8), "alloc evaluation");
+  CK(h->evOut.ensure(64), "alloc evaluation");
+  double* dout = h->evOut.as<double>();
+  int* bad = reinterpret_cast<int*>(dout + 4);
+  CK(fram::launch_evaluate(dA, dB, dF, dFt, (int)dt, n, F ? d : 0, static_cast<const int32_t*>(dP),
+                           h->evPart.as<double>(), dout, bad, st), "evaluate");
+  double hv[5];
+  CK(cudaMemcpyAsync(hv, dout, 5 * 8, cudaMemcpyDeviceToHost, st), "evaluation readback");
+  CK(cudaStreamSynchronize(st), "sync");
+  int hbad = 0;
+  memcpy(&hbad, &hv[4], sizeof(int));
+  if (hbad) return fail(FRAM_ERR_DATA, "perm entries must lie in [0, n)");
+  const double e_edges = 0.5 * std::sqrt(hv[0]), e_feat = std::sqrt(hv[1]);
+  out[0] = e_edges + e_feat;
+  out[1] = e_edges;
+  out[2] = e_feat;
+  out[3] = 0.5 * hv[2] + h->lambda * hv[3];
+  return FRAM_OK;
 }
 
 fram_status fram_get_unique_id(uint8_t id[128]) {

@@ -124,6 +124,10 @@ cudaError_t launch_init_n(double* N, void* Nq, int op, const double* X0, long ro
 // ---- K7: LAP (Alg.1 step 10, R17) --------------------------------------------------------------
 cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* work,
                        cudaStream_t st);
+// ---- K9: evaluation of a matching (Eq.1, matching error P:379); part: [n][4] FP64 workspace,
+// out (device): [Σ(A−MÃMᵀ)², Σ‖F−MF̃‖², Σ A∘MÃMᵀ, Σ⟨F, MF̃⟩]; *bad = 1 if perm is not in [0, n)
+cudaError_t launch_evaluate(const void* A, const void* B, const void* F, const void* Ft, int dt, long n, long d,
+                            const int32_t* perm, double* part, double* out, int* bad, cudaStream_t st);
 size_t lap_work_bytes(long n);
 size_t lap_err_offset(long n);     // byte offset of the LAP kernels' error word in the workspace (int, 0 = ok)
 

@@ -24,7 +24,8 @@ FLAG_TRACE, FLAG_CHECK_SYMMETRY, FLAG_NO_THETA_SCALE, FLAG_TIME_PHASES = 1, 2, 4
 
 EXPORTED = ["fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_destroy",
             "fram_last_error", "fram_get_unique_id", "fram_create_sharded", "fram_sdsn", "fram_gradient",
-            "fram_lap", "fram_abi_version", "fram_build_info", "fram_solve_attributed", "fram_create_sharded_virtual"]
+            "fram_lap", "fram_abi_version", "fram_build_info", "fram_solve_attributed", "fram_create_sharded_virtual",
+            "fram_evaluate"]
 
 
 class FramError(RuntimeError):
@@ -95,6 +96,7 @@ def lib():
     L.fram_get_unique_id.argtypes = [C.c_char_p]
     L.fram_create_sharded.argtypes = [i64, dbl, C.POINTER(_Schedule), C.c_char_p, C.c_int, C.c_int, C.c_int,
                                       C.POINTER(vp)]
+    L.fram_evaluate.argtypes = [vp, C.c_int, vp, vp, vp, vp, i64, vp, vp, C.POINTER(dbl)]
     L.fram_create_sharded_virtual.argtypes = [i64, dbl, C.POINTER(_Schedule), C.c_int, C.c_int, C.POINTER(vp)]
     L.fram_sdsn.argtypes = [vp, C.c_int, vp, vp, C.POINTER(i32), vp, vp]
     L.fram_gradient.argtypes = [vp, C.c_int, vp, vp, vp, vp, C.c_int, vp, vp, C.POINTER(dbl)]
@@ -104,7 +106,8 @@ def lib():
                                         vp, C.POINTER(_Stats)]
     for f in ("fram_create", "fram_set_schedule", "fram_solve", "fram_solve_batched", "fram_get_unique_id",
               "fram_solve_attributed",
-              "fram_create_sharded", "fram_create_sharded_virtual", "fram_sdsn", "fram_gradient", "fram_lap"):
+              "fram_create_sharded", "fram_create_sharded_virtual", "fram_sdsn", "fram_gradient", "fram_lap",
+              "fram_evaluate"):
         getattr(L, f).restype = C.c_int
     _lib_handle = L
     return L
@@ -317,6 +320,16 @@ def fram_lap(h: Handle, N, perm_out=None, stream=None):
     perm_out = _like(N, (h.n,), "i32") if perm_out is None else perm_out
     _check(lib().fram_lap(h.ptr, _ptr(N), _ptr(perm_out), _stream(stream, N)))
     return perm_out
+
+
+def fram_evaluate(h: Handle, A, B, perm, F=None, Ft=None, stream=None):
+    """Matching quality on the device (K9; Eq.(1)).  Returns dict(matching_error, edge_error,
+    feature_error, phi) for M[i, perm[i]] = 1 (perm int32, device or host)."""
+    out = (C.c_double * 4)()
+    d = 0 if F is None else int(F.shape[1])
+    _check(lib().fram_evaluate(h.ptr, _dt_of(A), _ptr(A), _ptr(B), _ptr(F), _ptr(Ft), d, _ptr(perm),
+                               _stream(stream, A), out))
+    return dict(matching_error=out[0], edge_error=out[1], feature_error=out[2], phi=out[3])
 
 
 def fram_get_unique_id() -> bytes:

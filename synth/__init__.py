@@ -13,6 +13,7 @@ from .graphs import (  # noqa: F401
     config_c3_batch,
     config_c4,
     config_c5,
+    config_ubc,
     ba_graph,
     er_graph,
     random_nonneg,

@@ -189,6 +189,40 @@ def config_c4(seed=0, n=4096):
     return Instance("C4", A, _permute(An, sigma), None, sigma.astype(np.int64), theta=10.0)
 
 
+def config_ubc(seed=0, n=2000, d=128, jitter=0.01, feat_noise=0.05):
+    """NEXT-2 stand-in for the paper's ubc(2000) task (Fig. 3; graphs from images App. F,
+    P:1047): FULLY CONNECTED keypoint graphs whose edge attribute is the inter-node Euclidean distance,
+    with SIFT-like node attributes.  The UBC images are not available; synthetic recipe:
+      points p_i ~ U[0,1]²; graph 2: q_{σ(i)} = R_φ p_i + τ + N(0, jitter² I) with a random rotation φ and
+      translation τ (a rigid motion keeps the distances); A_ij = ‖p_i − p_j‖, Ã_kl = ‖q_k − q_l‖;
+      features f_i = |z_i|/‖z_i‖, z_i ~ N(0, I_d) (non-negative, unit length like SIFT descriptors);
+      f̃_{σ(i)} = |f_i + N(0, feat_noise² I)| renormalised; K = F F̃ᵀ ≥ 0.
+    θ = 2 (dense graphs), λ = 1.  Returns an Instance with K = None and F, F̃ in meta."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    P = rng.random((n, 2))
+    phi = rng.uniform(0.0, 2.0 * np.pi)
+    Rm = np.array([[np.cos(phi), -np.sin(phi)], [np.sin(phi), np.cos(phi)]])
+    tau = rng.random(2)
+    Q0 = P @ Rm.T + tau + rng.normal(0.0, jitter, size=(n, 2))
+    sigma = rng.permutation(n)
+    Q = np.empty_like(Q0)
+    Q[sigma] = Q0
+    Z = np.abs(rng.normal(size=(n, d)))
+    F = Z / np.linalg.norm(Z, axis=1, keepdims=True)
+    G0 = np.abs(F + rng.normal(0.0, feat_noise, size=(n, d)))
+    G0 /= np.linalg.norm(G0, axis=1, keepdims=True)
+    Ft = np.empty_like(G0)
+    Ft[sigma] = G0
+
+    def dist(X):
+        D2 = ((X[:, None, :] - X[None, :, :]) ** 2).sum(-1)
+        return np.sqrt(np.maximum(D2, 0.0))
+
+    A = dist(P)
+    B = dist(Q)
+    return Instance("UBC", A, B, None, sigma.astype(np.int64), theta=2.0, meta={"F": F, "Ft": Ft})
+
+
 def _bf16_values(x):
     import torch
     return torch.from_numpy(np.asarray(x, np.float32)).to(torch.bfloat16).to(torch.float32).numpy()
