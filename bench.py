@@ -671,7 +671,8 @@ def run_ubc(args):
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": False,
             "dtype": dtype_label(args.precision), "data": "synthetic (synth.config_ubc: UBC ubc(2000) stand-in)",
             "config": {"workload": "UBC stand-in: n=2000 fully connected Euclidean-distance graphs, d=128 features, "
-                                   "theta=2, lambda=1", "n": n, "precision": args.precision, "schedule": SCHEDULE},
+                                   "theta=2, lambda=1", "n": n, "precision": args.precision,
+                       "schedule": dict(SCHEDULE, theta=inst.theta)},
             "mixed": main, "fp64": res["fp64"],
             "fp64_over_mixed_time_to_solution": res["fp64"]["time_to_solution_ms"] / main["time_to_solution_ms"],
             "paper_context": "12.7x mixed over GPU-FP64 on an RTX 4080 SUPER (P:551), whose FP64 rate is 1/64 of FP32"}

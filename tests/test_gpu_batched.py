@@ -4,8 +4,9 @@ import pytest
 import torch
 
 import oracle
-from paper_2508_00887_b200 import Schedule, fram_create, fram_solve_batched, FRAM_ERR_DATA
-from synth import config_c3_batch
+from paper_2508_00887_b200 import (Schedule, fram_create, fram_solve, fram_solve_batched, FRAM_ERR_DATA, FRAM_OK,
+                                   FRAM_NOT_CONVERGED)
+from synth import config_c2, config_c3_batch
 
 pytestmark = pytest.mark.gpu
 
@@ -110,3 +111,24 @@ def test_batched_small_n_ragged():
     for b, inst in enumerate(insts):
         ref = oracle.fram(inst.A, inst.B, None, theta=10.0, sdsn_fixed=40, delta_th=0.0, max_outer=5)
         assert np.max(np.abs(X[b].cpu().numpy() - ref["N"])) <= 1e-9
+
+
+@pytest.mark.parametrize("n,prec", [(100, "fp64"), (200, "tf32"), (512, "bf16")])
+def test_batched_above_64_matches_single_solves(n, prec):
+    # n > 64: the batch runs through the single-instance path on 4 worker streams; every instance must
+    # equal a standalone fram_solve of it bit for bit (same kernels, same inputs), and FP64 the oracle
+    insts = [config_c2(s, n=n) for s in range(6)]
+    dt = torch.float64 if prec == "fp64" else torch.float32
+    A = torch.tensor(np.stack([i.A for i in insts]), dtype=dt, device="cuda")
+    B = torch.tensor(np.stack([i.B for i in insts]), dtype=dt, device="cuda")
+    h = fram_create(n, schedule=Schedule(theta=10.0, max_outer=8))
+    st, stats, X, perm, sts = fram_solve_batched(h, A, B, precision=prec)
+    assert st in (FRAM_OK, FRAM_NOT_CONVERGED) and len(sts) == 6
+    for b, inst in enumerate(insts):
+        h1 = fram_create(n, schedule=Schedule(theta=10.0, max_outer=8))
+        s1, st1, X1, p1 = fram_solve(h1, A[b].contiguous(), B[b].contiguous(), precision=prec)
+        assert sts[b] == s1
+        assert torch.equal(X[b], X1) and torch.equal(perm[b], p1)
+        if prec == "fp64" and b < 2:
+            ref = oracle.fram(inst.A, inst.B, None, theta=10.0, replay=st1["passes"])
+            assert np.max(np.abs(X[b].cpu().numpy() - ref["N"])) <= 1e-9
