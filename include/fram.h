@@ -126,8 +126,10 @@ FRAM_API fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, con
                        const double* X0, fram_precision p, void* stream,
                        double* X_out, int32_t* perm_out, fram_stats* stats);
 
-/* `batch` independent solves of size n (handle's n ≤ 64) in one launch, one CTA per instance
- * (not in the paper).  Inputs are batch×n×n contiguous; X0 nullable;
+/* `batch` independent solves of size n (not in the paper).  n ≤ 64: one launch, one CTA
+ * per instance with the whole state on chip (K8).  n > 64: 4 worker threads with their own streams
+ * run the single-instance solve on the instances in turn (several instances on the GPU at once).
+ * Inputs are batch×n×n contiguous; X0 nullable;
  * status_out: int32[batch] per-instance fram_status (device or host), nullable; the call
  * returns the worst per-instance status.  stats (nullable) aggregates outer_iters (max),
  * total_passes (sum) and converged (1 iff all converged). */

@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <string>
 #include <thread>
@@ -88,7 +89,10 @@ struct fram_ctx {
   // graph and relaunched (NCCL communicators only; see sharded_solve)
   cudaGraphExec_t sh_graph = nullptr;
   cudaStream_t sh_cap_stream = nullptr;
-  bool sh_graph_off = false;        // capture failed once here: plain launches from then on
+  bool sh_graph_off = false;
+  // batched solves with n > 64: worker sub-handles, one host thread and stream each
+  std::vector<fram_ctx*> bsub;
+  std::vector<cudaStream_t> bstreams;        // capture failed once here: plain launches from then on
   unsigned char sh_graph_key[sizeof(fram::ShardSdsnParams) + 8] = {};
 };
 
@@ -670,6 +674,83 @@ fram_status group_solve(fram_ctx* g, int dt, const void* A, const void* B, const
   return st[0];
 }
 
+// Batched solves of instances larger than one CTA can hold (64 < n): P worker threads, each with its
+// own sub-handle and non-blocking stream, take instances from a shared counter and run the single-
+// instance solve on them (K4c one-cluster / K4r on-chip SDSN, LAP on one CTA or a cluster), so up to P
+// instances occupy the GPU at once.  Per-instance status in status_out; the worst status is returned.
+constexpr int kBatchWorkers = 4;
+fram_status batched_multi(fram_ctx* h, int64_t batch, int dt, const void* A, const void* B, const void* K,
+                          const double* X0, fram_precision p, cudaStream_t caller, double* X_out, int32_t* perm_out,
+                          int32_t* status_out, fram_stats* stats) {
+  const long n = h->n;
+  if (batch == 0) return FRAM_OK;
+  const int P = (int)std::min<int64_t>(kBatchWorkers, batch);
+  while ((int)h->bsub.size() < P) {
+    fram_handle sub = nullptr;
+    fram_status s = fram_create(n, h->lambda, &h->sched, h->device, &sub);
+    if (s != FRAM_OK) return s;
+    sub->dev_checked = h->dev_checked;
+    sub->num_sms = h->num_sms;
+    h->bsub.push_back(sub);
+    cudaStream_t cs = nullptr;
+    CK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "stream create");
+    h->bstreams.push_back(cs);
+  }
+  for (int w = 0; w < P; ++w) fram_set_schedule(h->bsub[w], &h->sched);
+  CK(cudaStreamSynchronize(caller), "caller stream sync");
+  const size_t es = dt_size(dt), mat = (size_t)n * n;
+  std::vector<int32_t> sts((size_t)batch, FRAM_OK);
+  std::vector<fram_stats> ist((size_t)batch);
+  std::vector<std::string> msg((size_t)batch);
+  std::atomic<int64_t> next{0};
+  auto work = [&](int w) {
+    fram_ctx* sub = h->bsub[w];
+    for (int64_t b = next++; b < batch; b = next++) {
+      fram_stats& s = ist[b];
+      s = fram_stats{};
+      const fram_status r = fram_solve(sub, (fram_dtype)dt, static_cast<const char*>(A) + b * mat * es,
+                                       static_cast<const char*>(B) + b * mat * es,
+                                       K ? static_cast<const char*>(K) + b * mat * es : nullptr,
+                                       X0 ? X0 + b * mat : nullptr, p, h->bstreams[w],
+                                       X_out ? X_out + b * mat : nullptr, perm_out ? perm_out + b * n : nullptr, &s);
+      sts[b] = r;
+      if (r != FRAM_OK && r != FRAM_NOT_CONVERGED) msg[b] = g_err;
+    }
+  };
+  std::vector<std::thread> th;
+  for (int w = 1; w < P; ++w) th.emplace_back(work, w);
+  work(0);
+  for (auto& t : th) t.join();
+  fram_status worst = FRAM_OK;
+  std::string wmsg;
+  int maxo = 0, allc = 1, capped = 0;
+  int64_t tot = 0, launches = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    const fram_status s = (fram_status)sts[b];
+    if (s != FRAM_OK && s != FRAM_NOT_CONVERGED) {
+      if (worst == FRAM_OK || worst == FRAM_NOT_CONVERGED) { worst = s; wmsg = msg[b]; }
+    } else if (s == FRAM_NOT_CONVERGED && worst == FRAM_OK) {
+      worst = FRAM_NOT_CONVERGED;
+    }
+    maxo = std::max(maxo, ist[b].outer_iters);
+    allc &= ist[b].converged;
+    capped += ist[b].sdsn_capped_calls;
+    tot += ist[b].total_passes;
+    launches += ist[b].kernel_launches;
+  }
+  if (status_out) CK(cudaMemcpy(status_out, sts.data(), (size_t)batch * 4, cudaMemcpyDefault), "status copy");
+  if (stats) {
+    stats->outer_iters = maxo;
+    stats->converged = allc;
+    stats->sdsn_capped_calls = capped;
+    stats->total_passes = tot;
+    stats->kernel_launches = launches;
+  }
+  if (worst == FRAM_NOT_CONVERGED) g_err = "one or more instances did not converge (status_out)";
+  else if (worst != FRAM_OK) g_err = "instance error (status_out): " + wmsg;
+  return worst;
+}
+
 }  // namespace
 
 extern "C" {
@@ -709,6 +790,8 @@ void fram_destroy(fram_handle h) {
   if (!h) return;
   cudaSetDevice(h->device);
   for (fram_ctx* sub : h->vsub) fram_destroy(sub);
+  for (fram_ctx* sub : h->bsub) fram_destroy(sub);
+  for (cudaStream_t s : h->bstreams) cudaStreamDestroy(s);
   for (cudaStream_t s : h->vstreams) cudaStreamDestroy(s);
   if (h->sh_graph) cudaGraphExecDestroy(h->sh_graph);
   if (h->sh_cap_stream) cudaStreamDestroy(h->sh_cap_stream);
@@ -953,6 +1036,9 @@ fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype dt, cons
   if (s0 != FRAM_OK) return s0;
   if (batch < 0 || !A || !B) return fail(FRAM_ERR_USAGE, "bad batch arguments");
   if (h->shard || !h->vsub.empty()) return fail(FRAM_ERR_USAGE, "not available on a sharded handle");
+  if (h->n > 64)
+    return batched_multi(h, batch, (int)dt, A, B, K, X0, p, reinterpret_cast<cudaStream_t>(stream), X_out, perm_out,
+                         status_out, stats);
   std::string err;
   fram_status s = fram::batched_solve(h->bws, h->n, h->lambda, h->sched, batch, (int)dt, A, B, K, X0, (int)p,
                                       reinterpret_cast<cudaStream_t>(stream), X_out, perm_out, status_out, stats,
