@@ -605,6 +605,16 @@ def run_c3(args):
                 "config": {"workload": "C3: 4096 x n=64 keypoint graphs, unary K, theta=2", "batch": total,
                            "precision": args.precision, "parallelism": f"instances split over {world} rank(s)"},
                 "outer_iters_max": stats["outer_iters"], "total_passes_rank0": stats["total_passes"],
+                # K8 keeps each instance's iterate in shared memory: per SDSN pass it reads and writes the
+                # 64x64 FP32 Y once (32 KB), so its ceiling is the SMEM bandwidth, 128 B/clk/SM (B200_PROFILING.md)
+                "roofline": {"kernel": "batched_kernel (K8, one CTA per instance)", "bound": "smem",
+                             "achieved": 2.0 * 4 * 64 * 64 * stats["total_passes"] * args.steps / (tot_ms / 1e3) / 1e9,
+                             "peak": 148 * 128 * 1.965e9 / 1e9, "unit": "GB/s",
+                             "frac": 2.0 * 4 * 64 * 64 * stats["total_passes"] * args.steps / (tot_ms / 1e3) / 1e9
+                             / (148 * 128 * 1.965e9 / 1e9),
+                             "traffic": None,
+                             "note": "SDSN-pass shared-memory bytes only (GEMMs, update, LAP excluded); the kernel is "
+                                     "latency / barrier bound at 2 CTAs per SM (DESIGN.md section 10)"},
                 "inlier_accuracy_rank0": acc, "gpu_launches": args.steps, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if world > 1:
