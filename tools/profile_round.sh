@@ -7,7 +7,7 @@ TAG=${1:-r01}
 OUT=gpurun_out
 mkdir -p $OUT
 timeout 900 python bench.py > $OUT/bench_${TAG}.json 2> $OUT/bench_${TAG}.err; echo "bench rc=$?"
-CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e"
+CMD="python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-extra-precisions"
 timeout 600 $CMD > $OUT/plain_${TAG}.log 2>&1 && \
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 700 --csv --log-file $OUT/launches_${TAG}.csv $CMD > $OUT/ncu_launch_${TAG}.log 2>&1; echo "launch list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:sdsn -s 3 -c 1 -o $OUT/prof_sdsn_${TAG} $CMD > $OUT/ncu_sdsn_${TAG}.log 2>&1; echo "ncu sdsn rc=$?"
