@@ -46,7 +46,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--precision", default="bf16", choices=["bf16", "tf32", "fp16", "fp64"])
-    p.add_argument("--n", type=int, default=4096, help="dev override (the metric is quoted at 4096)")
+    p.add_argument("--n", "--problem-size", dest="n", type=int, default=4096,
+                   help="dev override (the metric is quoted at 4096); use --problem-size under torchrun")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-extra-precisions", action="store_true",
