@@ -73,3 +73,12 @@ def test_virtual_shard_validation():
         with pytest.raises(fb.FramError) as e:
             fb.fram_create_sharded_virtual(n, 1.0, fb.Schedule(), world=w)
         assert e.value.status == fb.FRAM_ERR_USAGE
+
+
+def test_replay_longer_than_max_outer_is_usage_error():
+    # the stats trace arrays hold max_outer entries (include/fram.h): a longer replay is rejected up front
+    with pytest.raises(fb.FramError) as e:
+        fb.fram_create(16, schedule=fb.Schedule(max_outer=3, replay=[5, 5, 5, 5]))
+    assert e.value.status == fb.FRAM_ERR_USAGE
+    h = fb.fram_create(16, schedule=fb.Schedule(max_outer=4, replay=[5, 5, 5, 5]))
+    assert h.schedule.max_outer == 4

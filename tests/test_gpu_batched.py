@@ -132,3 +132,18 @@ def test_batched_above_64_matches_single_solves(n, prec):
         if prec == "fp64" and b < 2:
             ref = oracle.fram(inst.A, inst.B, None, theta=10.0, replay=st1["passes"])
             assert np.max(np.abs(X[b].cpu().numpy() - ref["N"])) <= 1e-9
+
+
+def test_batched_above_64_per_instance_status():
+    # one instance with a NaN: FRAM_ERR_DATA in its slot, the others solved normally
+    n = 96
+    insts = [config_c2(s, n=n) for s in range(3)]
+    A = np.stack([i.A for i in insts])
+    A[1, 5, 7] = np.nan
+    h = fram_create(n, schedule=Schedule(theta=10.0, max_outer=4))
+    st, stats, X, perm, sts = fram_solve_batched(h, torch.tensor(A, device="cuda"),
+                                                 torch.tensor(np.stack([i.B for i in insts]), device="cuda"),
+                                                 precision="fp64")
+    assert st == FRAM_ERR_DATA
+    assert sts[1] == FRAM_ERR_DATA and sts[0] in (FRAM_OK, FRAM_NOT_CONVERGED) and sts[2] in (FRAM_OK, FRAM_NOT_CONVERGED)
+    assert sorted(perm[0].cpu().numpy()) == list(range(n))

@@ -107,3 +107,12 @@ def test_virtual_shards_errors_do_not_hang():
     assert e.value.status == fb.FRAM_ERR_USAGE
     _, s, X, p = fb.fram_solve(h, _g(inst.A), _g(inst.B), precision="fp64")      # still usable
     assert sorted(p.cpu().numpy()) == list(range(256))
+
+
+def test_virtual_shards_host_buffers_match_device():
+    inst = config_c2(6, n=256)
+    h = fb.fram_create_sharded_virtual(256, 1.0, fb.Schedule(theta=inst.theta, max_outer=5), world=2)
+    _, s1, X1, p1 = fb.fram_solve(h, _g(inst.A), _g(inst.B), precision="fp64")
+    _, s2, X2, p2 = fb.fram_solve(h, np.ascontiguousarray(inst.A), np.ascontiguousarray(inst.B), precision="fp64")
+    assert isinstance(X2, np.ndarray) and np.array_equal(X1.cpu().numpy(), X2)
+    assert np.array_equal(p1.cpu().numpy(), p2) and s1["passes"] == s2["passes"]
