@@ -333,9 +333,13 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   };
 
   // one SDSN pass on one row slice: y ← max(0, (y + a_i) + b_j) (P2∘P1, R9 grouping) with paired
-  // FP32 adds (add.rn.f32x2: x+a, +b, column and row accumulation)
+  // FP32 adds (add.rn.f32x2: x+a, +b, column and row accumulation).  For CPT = 32 the row partial goes
+  // into two accumulators (alternate column pairs), halving its FADD2 dependency chain: 6.41 vs 6.58 µs
+  // per pass at n = 4096 (A/B on one B200, profiles/r02/ab_k4r_r02n.log; at CPT = 16 it measured 2%
+  // slower and four accumulators 7% slower at CPT = 32, so only CPT = 32 takes it)
+  constexpr bool kRs2 = (CPT == 32);
   auto pass_rows = [&](float (&x)[CH], float a, const float2 (&bv)[CH / 2], float2 (&col2)[CH / 2]) -> float {
-    float2 rs = make_float2(0.f, 0.f);
+    float2 rs = make_float2(0.f, 0.f), rs2 = make_float2(0.f, 0.f);
     const float2 a2 = make_float2(a, a);
 #pragma unroll
     for (int k = 0; k < CH; k += 2) {
@@ -345,8 +349,10 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
       x[k] = y.x;
       x[k + 1] = y.y;
       col2[k / 2] = add2(col2[k / 2], y);
-      rs = add2(rs, y);
+      if (kRs2 && ((k / 2) & 1)) rs2 = add2(rs2, y);
+      else rs = add2(rs, y);
     }
+    if (kRs2) rs = add2(rs, rs2);
     return rs.x + rs.y;
   };
   double abase = 0.0;                                    // 1/n + S/n² of the current pass
