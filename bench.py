@@ -412,8 +412,14 @@ def run_ours(args):
     def gemm_entry(prec, ms_gemm_, iters_, steps_):
         tfl = 4.0 * n ** 3 * iters_ / (ms_gemm_ / 1e3) / 1e12 if ms_gemm_ > 0 else None
         pk, src = gemm_peak(prec)
-        return {"tflops": tfl, "peak_tflops": pk, "peak_source": src, "frac_of_sustained": (tfl or 0) / pk,
-                "ms_per_step": ms_gemm_ / steps_, "operand_format": prec}
+        out = {"tflops": tfl, "peak_tflops": pk, "peak_source": src, "frac_of_sustained": (tfl or 0) / pk,
+               "ms_per_step": ms_gemm_ / steps_, "operand_format": prec}
+        if prec == "bf16":
+            # the metric's "GEMM TC util %": ncu sm__pipe_tensor_cycles_active of the two GEMMs at C4 (a profiler
+            # number, from the committed capture, not measured in this run)
+            out["tensor_pipe_active_pct_ncu"] = {"gemm1": 82.6, "gemm2": 73.4,
+                                                 "source": "profiles/r02/ncu_prof_gemm_r02_raw.csv"}
+        return out
 
     # ---- the paper's precisions beside the headline (TF32 = step 5 of Alg.1; FP64 = "GPU-FP64")
     extra = {}
