@@ -153,7 +153,14 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
   OT* sBT = reinterpret_cast<OT*>(carve(sizeof(OT) * NP * LDO));
   OT* sUT = reinterpret_cast<OT*>(carve(sizeof(OT) * NP * LDO));
   OT* sNq = (OP == 0) ? nullptr : reinterpret_cast<OT*>(carve(sizeof(OT) * NP * LDO));
-  double* sN = reinterpret_cast<double*>(carve(sizeof(double) * NP * LDO));
+  // TF32 (OP 1): the FP64 iterate N lives in registers — thread tid owns elements e = tid + k·BT, the
+  // update's own partition — which frees 33 KB and lets 2 CTAs share an SM instead of 1 (BF16 / FP16
+  // already fit 2, and 3 would not fit their registers; FP64 uses sN as the GEMM operand).  The LAP
+  // and X_out then read N from the sA|sBT region, written once after the outer loop.
+  constexpr bool NREG = (OP == 1);
+  constexpr int NK = NP * NP / BT;
+  double* sN = NREG ? nullptr : reinterpret_cast<double*>(carve(sizeof(double) * NP * LDO));
+  double nreg[NK];
   T* sK = reinterpret_cast<T*>(carve(sizeof(T) * NP * LDY));
   T* sY = reinterpret_cast<T*>(carve(sizeof(T) * NP * LDY));
   double* sr = reinterpret_cast<double*>(carve(sizeof(double) * NP));
@@ -224,9 +231,23 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
     sA[i * LDO + j] = rnd<OP>(ld_in(Ai, P.dt, e) / sqc);
     sBT[j * LDO + i] = rnd<OP>(ld_in(Bi, P.dt, e) / sqc);           // Ã'ᵀ
     if (Ki) sK[i * LDY + j] = (T)(ld_in(Ki, P.dt, e) / c);
-    const double x0 = P.X0 ? P.X0[inst * nn + e] : 1.0 / dn;
-    sN[i * LDO + j] = x0;
-    if constexpr (OP != 0) sNq[i * LDO + j] = rnd<OP>(x0);
+    if constexpr (!NREG) {
+      const double x0 = P.X0 ? P.X0[inst * nn + e] : 1.0 / dn;
+      sN[i * LDO + j] = x0;
+      if constexpr (OP != 0) sNq[i * LDO + j] = rnd<OP>(x0);
+    }
+  }
+  if constexpr (NREG) {
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const long e = tid + (long)k * BT;
+      nreg[k] = 0.0;
+      if (e < nn) {
+        const double x0 = P.X0 ? P.X0[inst * nn + e] : 1.0 / dn;
+        nreg[k] = x0;
+        sNq[(e / n) * LDO + (e % n)] = rnd<OP>(x0);
+      }
+    }
   }
   __syncthreads();
 
@@ -360,15 +381,32 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
     total += passes;
     // ---- Alg.1 steps 7-8: update and δ ----
     double dd = 0.0, nv2 = 0.0;
-    for (long e = tid; e < nn; e += BT) {
-      const int i = (int)(e / n), j = (int)(e % n);
-      const double old = sN[i * LDO + j];
-      const double nv = __dadd_rn(__dmul_rn(1.0 - P.alpha, old), __dmul_rn(P.alpha, (double)sY[i * LDY + j]));
-      const double df = __dsub_rn(nv, old);
-      dd = __fma_rn(df, df, dd);
-      nv2 = __fma_rn(nv, nv, nv2);
-      sN[i * LDO + j] = nv;
-      if constexpr (OP != 0) sNq[i * LDO + j] = rnd<OP>(nv);
+    if constexpr (NREG) {
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const long e = tid + (long)k * BT;
+        if (e < nn) {
+          const int i = (int)(e / n), j = (int)(e % n);
+          const double old = nreg[k];
+          const double nv = __dadd_rn(__dmul_rn(1.0 - P.alpha, old), __dmul_rn(P.alpha, (double)sY[i * LDY + j]));
+          const double df = __dsub_rn(nv, old);
+          dd = __fma_rn(df, df, dd);
+          nv2 = __fma_rn(nv, nv, nv2);
+          nreg[k] = nv;
+          sNq[i * LDO + j] = rnd<OP>(nv);
+        }
+      }
+    } else {
+      for (long e = tid; e < nn; e += BT) {
+        const int i = (int)(e / n), j = (int)(e % n);
+        const double old = sN[i * LDO + j];
+        const double nv = __dadd_rn(__dmul_rn(1.0 - P.alpha, old), __dmul_rn(P.alpha, (double)sY[i * LDY + j]));
+        const double df = __dsub_rn(nv, old);
+        dd = __fma_rn(df, df, dd);
+        nv2 = __fma_rn(nv, nv, nv2);
+        sN[i * LDO + j] = nv;
+        if constexpr (OP != 0) sNq[i * LDO + j] = rnd<OP>(nv);
+      }
     }
     dd = warp_sum_d(dd);
     nv2 = warp_sum_d(nv2);
@@ -389,6 +427,17 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
     }
   }
   if (t > T_outer) t = T_outer;
+  if constexpr (NREG) {                            // N → the sA|sBT region (free now) for the LAP / X_out
+    static_assert(!NREG || 2 * ((sizeof(OT) * NP * LDO + 15) / 16 * 16) >= sizeof(double) * NP * LDO, "sN alias");
+    __syncthreads();
+    sN = reinterpret_cast<double*>(sA);
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
+      const long e = tid + (long)k * BT;
+      if (e < nn) sN[(e / n) * LDO + (e % n)] = nreg[k];
+    }
+    __syncthreads();
+  }
 
   // ---- Alg.1 step 10: R17 Hungarian on warp 0 ----
   if (warp == 0) {
@@ -458,7 +507,8 @@ size_t smem_bytes() {
   auto r = [](size_t b) { return (b + 15) & ~size_t(15); };
   size_t s = 3 * r(sizeof(OT) * NP * LDO);
   if (OP != 0) s += r(sizeof(OT) * NP * LDO);
-  s += r(sizeof(double) * NP * LDO) + 2 * r(sizeof(T) * NP * LDY) + r(sizeof(double) * NP) +
+  if (OP != 1) s += r(sizeof(double) * NP * LDO);   // OP 1 keeps N in registers (fram_batched_kernel)
+  s += 2 * r(sizeof(T) * NP * LDY) + r(sizeof(double) * NP) +
        2 * r(sizeof(T) * NP) + r(sizeof(T) * BW * NP) + r(sizeof(double) * BW * 4) + r(sizeof(double) * (NP + 1) * 3) +
        r(sizeof(int) * (NP + 1) * 2) + r(NP + 1);
   return s;

@@ -72,10 +72,19 @@ def test_c4_fp64_free_running_reproduces_oracle(errlog):
     errlog("max|delta_gpu-delta_oracle|", dd, 1e-9, outer=stats["outer_iters"])
     assert dd <= 1e-9
     assert stats["converged"] == gold["converged"]
-    assert perm.cpu().numpy().tolist() == gold["perm"]
     Xn = X.cpu().numpy()
-    errlog("|sum N - oracle|", abs(Xn.sum() - gold["N_sum"]), 1e-6)
-    assert abs(Xn.sum() - gold["N_sum"]) <= 1e-6 and abs(np.linalg.norm(Xn) - gold["N_fro"]) <= 1e-9
+    errlog("|sum N - oracle|", abs(Xn.sum() - gold["N_sum"]), 1e-9)
+    assert abs(Xn.sum() - gold["N_sum"]) <= 1e-9 and abs(np.linalg.norm(Xn) - gold["N_fro"]) <= 1e-9
+    # the final N agrees to ~1e-13 (76 iterations of FP64 rounding in a different summation order), but the
+    # C4 N is flat (median row maximum 0.016) and such a perturbation can flip a near-tie of the LAP: the
+    # permutation is compared through Φ and accuracy (R19, R21); given the GPU's own N the LAP is bit-exact
+    p = perm.cpu().numpy()
+    phi = oracle.objective_perm(inst.A, inst.B, None, p)
+    rows = int((p != np.array(gold["perm"])).sum())
+    errlog("|dPhi|/Phi (fp64)", abs(phi - gold["phi_perm"]) / gold["phi_perm"], 1e-3, rows_differing=rows)
+    assert abs(phi - gold["phi_perm"]) <= 1e-3 * gold["phi_perm"]
+    assert abs(oracle.node_accuracy(p, inst.perm_true) - gold["accuracy"]) <= 0.005
+    assert np.array_equal(p, oracle.lap_max(Xn))
 
 
 def test_c4_fp64_replay_per_iteration_full_size(errlog):
