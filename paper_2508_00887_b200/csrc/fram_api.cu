@@ -283,13 +283,7 @@ int sdsn_kind(const fram_ctx* h, bool f64) {
 }
 bool use_resident(const fram_ctx* h, bool f64) { return sdsn_kind(h, f64) == 2; }
 
-#ifndef FRAM_DEV_NO_FUSED_UPDATE
-#define FRAM_DEV_NO_FUSED_UPDATE 0
-#endif
-// fuse_op > 0: the caller wants Alg.1 steps 7-8 (the update, operand format fuse_op) fused into the
-// SDSN launch; *fused reports whether the chosen kernel did it (K4r only)
-fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st, int fuse_op = 0, bool* fused = nullptr) {
-  if (fused) *fused = false;
+fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st) {
   double* scal = h->scal.as<double>();
   if (sdsn_kind(h, f64) == 4) {
     fram::SdsnParams p{};
@@ -331,16 +325,6 @@ fram_status run_sdsn(fram_ctx* h, bool f64, int fixed, cudaStream_t st, int fuse
     r.passes_out = reinterpret_cast<int*>(scal + 8);
     r.gamma_hist = h->ghist.as<double>();
     r.sdsn_out = scal;
-    if (fuse_op > 0 && !FRAM_DEV_NO_FUSED_UPDATE) {     // the update runs in the kernel's write-out (no D store)
-      r.Nupd = h->N.as<double>();
-      r.Nq = h->Nq.p;
-      r.upd_op = fuse_op;
-      r.alpha = h->sched.alpha;
-      r.upd_partials = h->upd.as<double>();
-      r.upd_counter = reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8);
-      r.upd_out3 = scal + 4;
-      if (fused) *fused = true;
-    }
 #if FRAM_DEV_RES_TIMING   // dev builds only (tools/build_variant.sh ... -DFRAM_DEV_RES_TIMING=1)
     {
       CK(h->rdbg.ensure((size_t)h->num_sms * 24 * 8), "alloc dbg");
@@ -878,16 +862,13 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     if ((rs = gradient(h, op, dK != nullptr, st)) != FRAM_OK) return rs;
     if (timing) CK(cudaEventRecord(h->ev[3], st), "event");
     const int fixed = replay ? h->replay[t - 1] : sc.sdsn_fixed;
-    bool fused = false;
-    if ((rs = run_sdsn(h, f64, fixed, st, f64 ? 0 : op, &fused)) != FRAM_OK) return rs;
+    if ((rs = run_sdsn(h, f64, fixed, st)) != FRAM_OK) return rs;
     if (timing) CK(cudaEventRecord(h->ev[4], st), "event");
-    if (!fused) {
-      CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, n, n, ld, sc.alpha, h->upd.as<double>(),
-                             reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8), scal + 4, st,
-                             h->num_sms),
-         "update");
-      h->launches++;
-    }
+    CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, n, n, ld, sc.alpha, h->upd.as<double>(),
+                           reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8), scal + 4, st,
+                           h->num_sms),
+       "update");
+    h->launches++;
     if (timing) CK(cudaEventRecord(h->ev[5], st), "event");
     CK(cudaMemcpyAsync(h->hscal, scal, kScalDoubles * 8, cudaMemcpyDeviceToHost, st), "scalar readback");
     CK(cudaStreamSynchronize(st), "iteration sync");

@@ -46,14 +46,6 @@ struct ResParams {
   int rs;              // rows per CTA held in shared memory (set by the launcher)
   int rmax;            // rows per CTA upper bound (set by the launcher)
   long long* dbg;      // dev-only (-DFRAM_DEV_RES_TIMING=1 builds): per-CTA phase times [grid][8]; null in the product
-  // fused Alg.1 steps 7-8 (the FRAM update, K5) in place of the D write-out; Nupd == null ⇒ write D to Y
-  double* Nupd;        // n×ld FP64 N, updated in place: N ← (1−α)N + αD (unfused, R15)
-  void* Nq;            // n×ld operand-format copy of the new N (op 1 tf32-as-fp32, 2 bf16, 3 fp16)
-  int upd_op;
-  double alpha;
-  double* upd_partials;  // [grid][2] per-CTA ΣΔ², ΣN²
-  unsigned* upd_counter; // zero on entry, reset by the last CTA
-  double* upd_out3;      // {ΣΔ², ΣN², δ}, written by the last CTA
 };
 int sdsn_res_grid(long n, int num_sms);       // 0 ⇒ n not supported on chip
 long sdsn_res_slots(long n);

@@ -598,80 +598,6 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
     P.dbg[b * 16 + 3] = tk2 - tk0;                                   // total ns to loop end
   }
 
-  if (P.Nupd) {
-    // ---------------- fused Alg.1 steps 7-8: N ← (1−α)N + αD, N_q, δ ----------------
-    // D never leaves the chip: each thread updates the N entries of its own rows and columns (FP64,
-    // unfused multiply/add as the update kernel K5 and the oracle, R15), stores N and its operand-format
-    // copy N_q, and accumulates ΣΔ², ΣN²; CTA partials are summed by the last CTA in CTA order.
-    const double alpha = P.alpha, oma = 1.0 - alpha;
-    double dd = 0.0, nn2 = 0.0;
-    auto upd1 = [&](double old, float d, double& nv) {
-      nv = __dadd_rn(__dmul_rn(oma, old), __dmul_rn(alpha, (double)d));
-      const double df = __dsub_rn(nv, old);
-      dd = __fma_rn(df, df, dd);
-      nn2 = __fma_rn(nv, nv, nn2);
-    };
-    auto store_q = [&](long idx, double v) {
-      if (P.upd_op == 2) reinterpret_cast<__nv_bfloat16*>(P.Nq)[idx] = __double2bfloat16(v);
-      else if (P.upd_op == 3) reinterpret_cast<__half*>(P.Nq)[idx] = __double2half(v);
-      else reinterpret_cast<float*>(P.Nq)[idx] = tf32_rne(__double2float_rn(v));
-    };
-    for (int r = g; r < R; r += 2) {
-      float x[CH];
-      load_row(r, x);
-      double* nrow = P.Nupd + (r0 + r) * ld;
-      const long qrow = (r0 + r) * ld;
-#pragma unroll
-      for (int c = 0; c < VH; ++c) {
-        const long col = (long)t * CPT + 4 * (c0 + c);
-        if (col + 3 < n) {
-          const double2 o0 = *reinterpret_cast<const double2*>(nrow + col);
-          const double2 o1 = *reinterpret_cast<const double2*>(nrow + col + 2);
-          double2 v0, v1;
-          upd1(o0.x, x[4 * c], v0.x);
-          upd1(o0.y, x[4 * c + 1], v0.y);
-          upd1(o1.x, x[4 * c + 2], v1.x);
-          upd1(o1.y, x[4 * c + 3], v1.y);
-          *reinterpret_cast<double2*>(nrow + col) = v0;
-          *reinterpret_cast<double2*>(nrow + col + 2) = v1;
-          store_q(qrow + col, v0.x); store_q(qrow + col + 1, v0.y);
-          store_q(qrow + col + 2, v1.x); store_q(qrow + col + 3, v1.y);
-        } else {
-#pragma unroll
-          for (int e4 = 0; e4 < 4; ++e4)
-            if (col + e4 < n) {
-              double nv;
-              upd1(nrow[col + e4], x[4 * c + e4], nv);
-              nrow[col + e4] = nv;
-              store_q(qrow + col + e4, nv);
-            }
-        }
-      }
-    }
-    dd = warp_sum_d(dd);
-    nn2 = warp_sum_d(nn2);
-    __shared__ bool s_last;
-    if (lane == 0) { s_red2[0][warp] = dd; s_red2[1][warp] = nn2; }
-    __syncthreads();
-    if (tid == 0) {
-      double a = 0.0, c2 = 0.0;
-      for (int w = 0; w < NW; ++w) { a += s_red2[0][w]; c2 += s_red2[1][w]; }
-      P.upd_partials[2 * b] = a;
-      P.upd_partials[2 * b + 1] = c2;
-      __threadfence();
-      s_last = atomicAdd(P.upd_counter, 1u) == (unsigned)(G - 1);
-    }
-    __syncthreads();
-    if (s_last && tid == 0) {
-      __threadfence();
-      double a = 0.0, c2 = 0.0;
-      for (int k = 0; k < G; ++k) { a += __ldcg(P.upd_partials + 2 * k); c2 += __ldcg(P.upd_partials + 2 * k + 1); }
-      P.upd_out3[0] = a;
-      P.upd_out3[1] = c2;
-      P.upd_out3[2] = sqrt(a) / sqrt(c2);
-      *P.upd_counter = 0u;
-    }
-  } else {
   // ---------------- D = Y_final → global (row-major, ld) ----------------
   for (int r = g; r < R; r += 2) {
     float x[CH];
@@ -688,7 +614,6 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
         if (col + 2 < n) grow[col + 2] = x[4 * c + 2];
       }
     }
-  }
   }
   if (b == 0 && tid == 0) {
     *P.passes_out = j + 1;
