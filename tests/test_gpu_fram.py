@@ -153,3 +153,22 @@ def test_fram_tiny_sizes(n, prec):
         assert np.array_equal(p, ref["perm"])
     if n == 1:
         assert p[0] == 0 and abs(Xn[0, 0] - 1.0) <= 1e-6
+
+
+def test_fram_above_on_chip_limit_bf16():
+    # n = 5000 > 4096: the FP32 SDSN streams through L2/HBM (K4) and the LAP runs on the 4-CTA cluster with
+    # 8 columns per thread; a few outer iterations, output properties and the bit-exact LAP of the GPU's N
+    rng = np.random.Generator(np.random.PCG64(5000))
+    n = 5000
+    from synth import ba_graph
+    A = ba_graph(rng, n, 3)
+    sig = rng.permutation(n)
+    B = np.empty_like(A)
+    B[np.ix_(sig, sig)] = A
+    h = fram_create(n, schedule=Schedule(theta=10.0, max_outer=3, sdsn_max=50))
+    st, stats, X, perm = fram_solve(h, _g(A, torch.float32), _g(B, torch.float32), precision="bf16")
+    assert st in (FRAM_OK, FRAM_NOT_CONVERGED) and stats["sdsn_kernel"] == 1 and stats["passes"] == [50, 50, 50]
+    Xn = X.cpu().numpy()
+    assert np.all(Xn >= 0)
+    p = perm.cpu().numpy()
+    assert np.array_equal(p, oracle.lap_max(Xn))
