@@ -21,6 +21,14 @@
 #include "common.cuh"
 #include "internal.h"
 
+// The records arrive by st.async in this CTA's own shared memory and complete on this CTA's mbarrier,
+// so observing the phase with the default (CTA-scope acquire) semantics orders the reads after the
+// data; ".acquire.cluster" made ptxas add an L1 invalidation (CCTL.IVALL) to every wait: 87.6 → 84.6 ms
+// for the C4 LAP without it (profiles/r02/ab_mbar.log).
+#ifndef MBAR_SEM
+#define MBAR_SEM ""
+#endif
+
 namespace fram {
 namespace {
 
@@ -326,7 +334,7 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
       {                                               // wait for all CS·16 records of this step
         uint32_t done = 0;
         while (!done)
-          asm volatile("{ .reg .pred pp; mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 pp, [%1], %2; selp.u32 %0, 1, 0, pp; }"
+          asm volatile("{ .reg .pred pp; mbarrier.try_wait.parity" MBAR_SEM ".shared::cta.b64 pp, [%1], %2; selp.u32 %0, 1, 0, pp; }"
                        : "=r"(done) : "r"(mb0 + 8 * q), "r"(ph) : "memory");
       }
       uint64_t dkey = ~0ull;
