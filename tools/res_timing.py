@@ -1,5 +1,6 @@
 """Dev probe: K4r on a 5%-dense random n=4096 input, 1000 fixed passes; prints ms per call (CUDA events).
-With FRAM_RES_TIMING=1 the library also prints its per-phase globaltimer breakdown (perturbs timing)."""
+With a -DFRAM_DEV_RES_TIMING=1 variant of fram_api.cu (tools/build_variant.sh) the library also prints its
+per-phase globaltimer breakdown (perturbs timing)."""
 import os
 import sys
 

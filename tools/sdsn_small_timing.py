@@ -1,5 +1,6 @@
-"""Dev probe: SDSN time per pass at small n for the kernel the library picks (set FRAM_SDSN_NOCLUSTER=1
-or FRAM_SDSN_STREAM=1 to compare K4r / K4)."""
+"""Dev probe: SDSN time per pass at small n for the kernel the library picks (compare K4r / K4 with
+variant libraries: bash tools/build_variant.sh <name> fram_api.cu -DFRAM_DEV_NOCLUSTER=1 or
+-DFRAM_DEV_FORCE_STREAM=1, then bash tools/ab.sh python tools/sdsn_small_timing.py)."""
 import os
 import sys
 

@@ -1,4 +1,5 @@
-"""Dev probe: streaming SDSN (K4) per-pass time at n=4096 in FP64 (and FP32 with FRAM_SDSN_STREAM=1)."""
+"""Dev probe: streaming SDSN (K4) per-pass time at n=4096 in FP64 (FP32 with a -DFRAM_DEV_FORCE_STREAM=1
+variant of fram_api.cu, tools/build_variant.sh)."""
 import os
 import sys
 
