@@ -182,11 +182,12 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
       colacc[m2] = (T)0;
       bl[m2] = (mode && j < n) ? s_b[j] : (T)0;           // b of my columns, for every row
     }
-    for (int i = warp; i < R; i += kCWarps) {
+    // one row of this warp: y ← op(y) on the lane's ≤ MC columns, column partials, returns the lane's
+    // row partial.  Loads, arithmetic and stores in separate unrolled loops (no branch between columns,
+    // so the columns' dependency chains overlap); columns ≥ n read and contribute 0
+    auto row = [&](int i) -> T {
       const T a = mode ? s_a[i] : (T)0;
       T rs = (T)0;
-      // loads, arithmetic and stores in separate unrolled loops (no branch between columns, so the
-      // columns' dependency chains overlap); columns ≥ n read and contribute 0
       T xv[MC];
 #pragma unroll
       for (int m2 = 0; m2 < MC; ++m2) {
@@ -213,10 +214,55 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
         const int j = lane + 32 * m2;
         if (j < n) Ys[i * ldn + j] = xv[m2];
       }
-      double r;
-      if constexpr (sizeof(T) == 8) r = warp_sum_d((double)rs);
-      else r = (double)warp_sum_f((float)rs);
-      if (lane == 0) {
+      return rs;
+    };
+    // n > 32 (R = 32 rows, 4 per warp): the warp's row partials are reduced together by one transpose-
+    // reduce after its rows (5-9% faster per pass at n = 64-500, profiles/r02/ab_k4c4.log); n ≤ 32 (one
+    // CTA, ≤ 3 rows per warp): row by row, as before
+    constexpr int RB = kCMaxRows / kCWarps;             // 8
+    constexpr bool batch_rows = MC > 1;
+    T rsv[RB];
+    if constexpr (batch_rows) {
+#pragma unroll
+      for (int q = 0; q < RB; ++q) rsv[q] = (T)0;
+#pragma unroll
+      for (int q = 0; q < RB; ++q) {
+        const int i = warp + q * kCWarps;
+        if (i >= R) break;
+        rsv[q] = row(i);
+      }
+    } else {
+      for (int i = warp; i < R; i += kCWarps) {
+        const T rs = row(i);
+        double r;
+        if constexpr (sizeof(T) == 8) r = warp_sum_d((double)rs);
+        else r = (double)warp_sum_f((float)rs);
+        if (lane == 0) {
+          s_r[i] = r;
+          s_rn[i] = div_n(r, dn, rn);
+        }
+      }
+    }
+    if constexpr (batch_rows) {   // transpose-reduce of the RB = 8 rows: xor 16, 8, 4 halve the rows a
+      // lane carries, xor 2, 1 finish; lane 4q ends with row q's sum (fixed tree, deterministic; FP64 adds
+      // for T = double, FP32 partials then FP64 for T = float as before)
+      using A = typename std::conditional<sizeof(T) == 8, double, float>::type;
+      A v[RB];
+#pragma unroll
+      for (int q = 0; q < RB; ++q) v[q] = (A)rsv[q];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const int off = 16 >> l, m = RB >> (l + 1);
+        const bool hi = lane & off;
+#pragma unroll
+        for (int q = 0; q < m; ++q) v[q] = (hi ? v[q + m] : v[q]) + __shfl_xor_sync(0xffffffffu, hi ? v[q] : v[q + m], off);
+      }
+      A z = v[0];
+      z += __shfl_xor_sync(0xffffffffu, z, 2);
+      z += __shfl_xor_sync(0xffffffffu, z, 1);
+      const int i = warp + (lane >> 2) * kCWarps;
+      if ((lane & 3) == 0 && i < R) {
+        const double r = (double)z;
         s_r[i] = r;
         s_rn[i] = div_n(r, dn, rn);
       }
@@ -247,11 +293,29 @@ __global__ void __launch_bounds__(kCThreads, 1) sdsn_cluster_kernel(SdsnParams P
     }
     mb_wait(mb0, par);                                   // my slice's partials and every mass arrived
     S = 0.0;                                             // every CTA: the masses in CTA order
-    for (int k = 0; k < C; ++k) S += s_Sp[par][k];
+    if constexpr (MC > 1) {
+      double mv[kCMaxCluster];
+#pragma unroll
+      for (int k = 0; k < kCMaxCluster; ++k) mv[k] = k < C ? s_Sp[par][k] : 0.0;
+#pragma unroll
+      for (int k = 0; k < kCMaxCluster; ++k)
+        if (k < C) S += mv[k];
+    } else {
+      for (int k = 0; k < C; ++k) S += s_Sp[par][k];
+    }
     // my column slice: c_j = Σ over CTAs in order (FP64); b_j = −c_j/n → every CTA (DSMEM)
     for (int j = k0 + tid; j < k1; j += kCThreads) {
       double cs = 0.0;
-      for (int k = 0; k < C; ++k) cs += (double)s_recv[k * SL + (j - k0)];
+      if constexpr (MC > 1) {
+        T pv[kCMaxCluster];                             // all loads in flight, then the sum in CTA order
+#pragma unroll
+        for (int k = 0; k < kCMaxCluster; ++k) pv[k] = k < C ? s_recv[k * SL + (j - k0)] : (T)0;
+#pragma unroll
+        for (int k = 0; k < kCMaxCluster; ++k)
+          if (k < C) cs += (double)pv[k];
+      } else {                                          // n ≤ 32: one CTA
+        for (int k = 0; k < C; ++k) cs += (double)s_recv[k * SL + (j - k0)];
+      }
       const T bj = (T)(-div_n(cs, dn, rn));
       for (int k = 0; k < C; ++k) {
         ast_t<T>(dsmem(&s_b[j], (unsigned)k), bj, dsmem(&s_mb[1], (unsigned)k));
