@@ -470,12 +470,17 @@ cudaError_t launch_lap(const double* N, long n, long ld, int32_t* perm, void* wo
   if (n <= 256) return launch_t<256, 1>(N, n, ld, perm, work, st);
   if (n <= 512) return launch_t<512, 1>(N, n, ld, perm, work, st);
   if (n <= 1024) return launch_t<512, 2>(N, n, ld, perm, work, st);
-  if (n <= 2048) return launch_t<512, 4>(N, n, ld, perm, work, st);
+  // 1024 < n ≤ 2048: a cluster of 4 CTAs × 128 threads × 4 columns (round 2: 40.2 vs 47.6 ms on one CTA
+  // for a flat n = 2000 N, 2.1 vs 1.9 ms on a near-permutation one; profiles/r02/ab_lapsizes.log)
+  if (n <= 2048) return launch_cluster_t<4, 4, 128>(N, n, ld, perm, work, st);
   // 2048 < n ≤ 8192: a cluster of 4 CTAs × 256 threads (C4, n = 4096: 86.7 ms against 120.0 ms on
   // one CTA; measured 2/4/8/16 CTAs × 128–1024 threads: 86.7–125 ms); the replicated u/p/way/tree arrays
   // (20 B per row) must fit in shared memory
-  if (n <= 4096) return launch_cluster_t<4, 4, 256>(N, n, ld, perm, work, st);
-  if (n <= 8192) return launch_cluster_t<4, 8, 256>(N, n, ld, perm, work, st);
+  // n ≤ 4096: 8 CTAs × 128 threads × 4 columns (round 2, after the deferred potentials and the CTA-scope
+  // record wait: 82.2 ms at C4 against 84.6 ms for 4 × 256 × 4; 2/4/8/16 CTAs × 64-512 threads measured
+  // 82.2-107.7 ms, profiles/r02/ab_lapcfg*.log)
+  if (n <= 4096) return launch_cluster_t<8, 4, 128>(N, n, ld, perm, work, st);
+  if (n <= 8192) return launch_cluster_t<8, 8, 128>(N, n, ld, perm, work, st);   // 3% faster than 4 × 256 (r02)
   // n ≤ 16384: 8 CTAs × 256 threads × 8 columns, u in global memory (4×16 and 16×4 measured slower)
   if (n <= 16384) return launch_cluster_t<8, 8, 256, true>(N, n, ld, perm, work, st);
   if (n <= 65536) return launch_t<1024, 64>(N, n, ld, perm, work, st);
