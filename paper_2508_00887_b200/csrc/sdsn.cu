@@ -81,7 +81,12 @@ template <> __device__ __forceinline__ float4 vmake<float>(const float* o) { ret
 template <> __device__ __forceinline__ double2 vmake<double>(const double* o) { return make_double2(o[0],o[1]); }
 
 __device__ __forceinline__ float tmax0(float x) { return fmaxf(0.0f, x); }
-__device__ __forceinline__ double tmax0(double x) { return fmax(0.0, x); }
+// max(0, x) for FP64 by the sign bit (3 integer ops; fmax is a DSETP on the FP64 pipe plus 4-5
+// selects for its NaN / signed-zero rules, which finite iterates never need: −0 → +0 either way)
+__device__ __forceinline__ double tmax0(double x) {
+  const long long v = __double_as_longlong(x);
+  return __longlong_as_double(v & ~(v >> 63));
+}
 __device__ __forceinline__ float warp_sum_t(float v) { return warp_sum_f(v); }
 __device__ __forceinline__ double warp_sum_t(double v) { return warp_sum_d(v); }
 
@@ -287,8 +292,83 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
 #pragma unroll
     for (int s = 0; s < PD; ++s)
       if (s < nrs) load_row(s, s);
-    // on-chip rows: one at a time (TMEM or shared memory; the scale sweep reads X from global)
-    for (int il = 0; il < non; ++il) {
+    // on-chip rows: one at a time (TMEM or shared memory; the scale sweep reads X from global).  The
+    // TMEM and shared-memory rows are separate code paths and full rows skip the ragged-tail tests:
+    // one shared register array with per-element tail checks cost ~330 instructions per row and
+    // warp (ncu source page, FP64 n = 4096: the on-chip rows took as long as the streamed ones).
+    auto onchip = [&](auto full_c, int il) {
+      constexpr bool FULL = decltype(full_c)::value;
+      const T a = (mode_c.value == SWEEP_PASS) ? s_a[il] : (T)0;
+      VT* row = Yc + il * ldv;
+      auto body = [&](VT (&v)[VPL]) -> T {
+        T r = (T)0;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          if (FULL || kindf(k)) {
+            T x[W], bb[W];
+            vget<T>(v[k], x);
+            getb(k, bb);
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+              T y;
+              if constexpr (decltype(mode_c)::value == SWEEP_PASS) y = tmax0((x[w] + a) + bb[w]);
+              else y = P.scale ? (T)(sc * (double)x[w]) : x[w];
+              if (!FULL && kindf(k) == 2 && qvf(k) * W + w >= (int)n) y = (T)0;
+              x[w] = y;
+              r += y;
+            }
+            cadd(k, x);
+            v[k] = vmake<T>(x);
+          }
+        }
+        return r;
+      };
+      T r;
+      if (mode_c.value == SWEEP_SCALE || il >= NT) {
+        VT v[VPL];
+        VT* src = il >= NT ? s_on + (long)(il - NT) * nvec : nullptr;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (FULL || kindf(k)) v[k] = mode_c.value == SWEEP_SCALE ? __ldcg(row + qvf(k)) : src[qvf(k)];
+        r = body(v);
+        if (wb) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k)
+            if (FULL || kindf(k)) __stcg(row + qvf(k), v[k]);
+        }
+        if (il < NT) {
+          uint32_t wv[WPR];
+#pragma unroll
+          for (int k = 0; k < VPL; ++k) *reinterpret_cast<VT*>(&wv[k * (WPR / VPL)]) = v[k];
+          tmem_st<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
+        } else {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k)
+            if (FULL || kindf(k)) s_on[(long)(il - NT) * nvec + qvf(k)] = v[k];
+        }
+      } else {
+        uint32_t wv[WPR];
+        tmem_ld<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
+        tmem_wait_ld();
+        VT v[VPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) v[k] = *reinterpret_cast<const VT*>(&wv[k * (WPR / VPL)]);
+        r = body(v);
+        if (wb) {
+#pragma unroll
+          for (int k = 0; k < VPL; ++k)
+            if (FULL || kindf(k)) __stcg(row + qvf(k), v[k]);
+        }
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) *reinterpret_cast<VT*>(&wv[k * (WPR / VPL)]) = v[k];
+        tmem_st<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
+      }
+      r = warp_sum_t(r);
+      if (lane == 0) s_rowpart[il * CG + cg] = (double)r;
+    };
+    // FP32 on-chip rows: the round-1 row body (one register array for TMEM / shared memory /
+    // global words; the split body below measured slower for FP32: n = 16384 354 → 436 us/pass)
+    auto onchip32 = [&](int il) {
       // one register array holds the row slice: TMEM words, shared-memory or global vectors
       uint32_t wv[WPR];
       VT* row = Yc + il * ldv;
@@ -331,9 +411,16 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       if (il < NT) tmem_st<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), wv);
       r = warp_sum_t(r);
       if (lane == 0) s_rowpart[il * CG + cg] = (double)r;
-    }
+    };
+    // FP64: the split row body inside the full / ragged dispatch (with the sign-bit max: FP64
+    // n = 4096 26.7 → 22.1 us/pass, n = 2048 10.2 → 7.5; `profiles/r02/ab_k4lean2.log`)
+    constexpr bool kF64Body = sizeof(T) == 8;
+    if constexpr (!kF64Body)
+      for (int il = 0; il < non; ++il) onchip32(il);
     auto run = [&](auto full_c) {
       constexpr bool FULL = decltype(full_c)::value;
+      if constexpr (kF64Body)
+        for (int il = 0; il < non; ++il) onchip(full_c, il);
       for (int base = 0; base < nrs; base += PD) {
         T rs[PD];
 #pragma unroll
