@@ -66,6 +66,9 @@ template <typename T> struct VecT;
 template <> struct VecT<float>  { using t = float4;  static constexpr int W = 4; };
 template <> struct VecT<double> { using t = double2; static constexpr int W = 2; };
 
+#ifndef SDSN_PAIR
+#define SDSN_PAIR 1
+#endif
 #ifndef SDSN_ONCHIP
 #define SDSN_ONCHIP 1
 #endif
@@ -92,7 +95,10 @@ __device__ __forceinline__ double warp_sum_t(double v) { return warp_sum_d(v); }
 
 enum { SWEEP_SCALE = 0, SWEEP_PASS = 1 };
 
-template <typename T, int VPL>
+// OO ("on-chip only"): every row of every CTA is held in TMEM / shared memory (FP64, n ≲ 2070 on 148
+// SMs); that instantiation has no streamed-row loop and takes the on-chip rows in pairs, which the
+// streamed-row loop's registers do not allow (FP64 n = 4096 with pairs: 22.1 → 41.4 us/pass)
+template <typename T, int VPL, bool OO>
 __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int CG, int NT, int NSM) {
   using VT = typename VecT<T>::t;
   constexpr int W = VecT<T>::W;
@@ -276,7 +282,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     // rev: the streamed rows in reverse order (odd passes), so a pass starts on the rows the
     // previous pass wrote last — still in L2 when they are about the L2 size
     const int non = RG == 1 ? min(NT + NSM, nrw) : 0;
-    const int nrs = nrw - non;
+    const int nrs = OO ? 0 : nrw - non;
     auto rmap = [&](int rr) { return non + (rev ? nrs - 1 - rr : rr); };
     auto load_row = [&](int s, int rr) {
       const VT* row = Yc + (rg + rmap(rr) * RG) * ldv;
@@ -296,33 +302,34 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
     // TMEM and shared-memory rows are separate code paths and full rows skip the ragged-tail tests:
     // one shared register array with per-element tail checks cost ~330 instructions per row and
     // warp (ncu source page, FP64 n = 4096: the on-chip rows took as long as the streamed ones).
+  auto rowbody = [&](auto full_c, VT (&v)[VPL], T a) -> T {
+    constexpr bool FULL = decltype(full_c)::value;
+      T r = (T)0;
+#pragma unroll
+      for (int k = 0; k < VPL; ++k) {
+        if (FULL || kindf(k)) {
+          T x[W], bb[W];
+          vget<T>(v[k], x);
+          getb(k, bb);
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            T y;
+            if constexpr (decltype(mode_c)::value == SWEEP_PASS) y = tmax0((x[w] + a) + bb[w]);
+            else y = P.scale ? (T)(sc * (double)x[w]) : x[w];
+            if (!FULL && kindf(k) == 2 && qvf(k) * W + w >= (int)n) y = (T)0;
+            x[w] = y;
+            r += y;
+          }
+          cadd(k, x);
+          v[k] = vmake<T>(x);
+        }
+      }
+      return r;
+    };
     auto onchip = [&](auto full_c, int il) {
       constexpr bool FULL = decltype(full_c)::value;
       const T a = (mode_c.value == SWEEP_PASS) ? s_a[il] : (T)0;
       VT* row = Yc + il * ldv;
-      auto body = [&](VT (&v)[VPL]) -> T {
-        T r = (T)0;
-#pragma unroll
-        for (int k = 0; k < VPL; ++k) {
-          if (FULL || kindf(k)) {
-            T x[W], bb[W];
-            vget<T>(v[k], x);
-            getb(k, bb);
-#pragma unroll
-            for (int w = 0; w < W; ++w) {
-              T y;
-              if constexpr (decltype(mode_c)::value == SWEEP_PASS) y = tmax0((x[w] + a) + bb[w]);
-              else y = P.scale ? (T)(sc * (double)x[w]) : x[w];
-              if (!FULL && kindf(k) == 2 && qvf(k) * W + w >= (int)n) y = (T)0;
-              x[w] = y;
-              r += y;
-            }
-            cadd(k, x);
-            v[k] = vmake<T>(x);
-          }
-        }
-        return r;
-      };
       T r;
       if (mode_c.value == SWEEP_SCALE || il >= NT) {
         VT v[VPL];
@@ -330,7 +337,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
 #pragma unroll
         for (int k = 0; k < VPL; ++k)
           if (FULL || kindf(k)) v[k] = mode_c.value == SWEEP_SCALE ? __ldcg(row + qvf(k)) : src[qvf(k)];
-        r = body(v);
+        r = rowbody(full_c, v, a);
         if (wb) {
 #pragma unroll
           for (int k = 0; k < VPL; ++k)
@@ -353,7 +360,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
         VT v[VPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) v[k] = *reinterpret_cast<const VT*>(&wv[k * (WPR / VPL)]);
-        r = body(v);
+        r = rowbody(full_c, v, a);
         if (wb) {
 #pragma unroll
           for (int k = 0; k < VPL; ++k)
@@ -365,6 +372,70 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       }
       r = warp_sum_t(r);
       if (lane == 0) s_rowpart[il * CG + cg] = (double)r;
+    };
+    // two on-chip rows of the same kind at once (PASS sweeps): independent chains for the TMEM / shared-
+    // memory latency and the FP64 adds, and one paired warp reduction (xor 16 splits the two rows
+    // between the half-warps: 5 shuffle rounds for both rows instead of 10)
+    auto onchip2 = [&](auto full_c, int il) {
+      constexpr bool FULL = decltype(full_c)::value;
+      const T a0 = s_a[il], a1 = s_a[il + 1];
+      VT v0[VPL], v1[VPL];
+      if (il < NT) {
+        uint32_t w0[WPR], w1[WPR];
+        tmem_ld<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), w0);
+        tmem_ld<WPR>(tmem + (uint32_t)(((il + 1) * 4 + (warp >> 2)) * WPR), w1);
+        tmem_wait_ld();
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          v0[k] = *reinterpret_cast<const VT*>(&w0[k * (WPR / VPL)]);
+          v1[k] = *reinterpret_cast<const VT*>(&w1[k * (WPR / VPL)]);
+        }
+      } else {
+        const VT* s0 = s_on + (long)(il - NT) * nvec;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (FULL || kindf(k)) { v0[k] = s0[qvf(k)]; v1[k] = s0[nvec + qvf(k)]; }
+      }
+      T r0 = rowbody(full_c, v0, a0);
+      T r1 = rowbody(full_c, v1, a1);
+      if (wb) {
+        VT* row0 = Yc + il * ldv;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (FULL || kindf(k)) { __stcg(row0 + qvf(k), v0[k]); __stcg(row0 + ldv + qvf(k), v1[k]); }
+      }
+      if (il < NT) {
+        uint32_t w0[WPR], w1[WPR];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) {
+          *reinterpret_cast<VT*>(&w0[k * (WPR / VPL)]) = v0[k];
+          *reinterpret_cast<VT*>(&w1[k * (WPR / VPL)]) = v1[k];
+        }
+        tmem_st<WPR>(tmem + (uint32_t)((il * 4 + (warp >> 2)) * WPR), w0);
+        tmem_st<WPR>(tmem + (uint32_t)(((il + 1) * 4 + (warp >> 2)) * WPR), w1);
+      } else {
+        VT* s0 = s_on + (long)(il - NT) * nvec;
+#pragma unroll
+        for (int k = 0; k < VPL; ++k)
+          if (FULL || kindf(k)) { s0[qvf(k)] = v0[k]; s0[nvec + qvf(k)] = v1[k]; }
+      }
+      const bool hi = (lane & 16) != 0;
+      T keep = hi ? r1 : r0;
+      keep += __shfl_xor_sync(0xffffffffu, hi ? r0 : r1, 16);
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, o);
+      if ((lane & 15) == 0) s_rowpart[(il + (hi ? 1 : 0)) * CG + cg] = (double)keep;
+    };
+    // the on-chip rows of a PASS sweep: pairs within the TMEM rows, then within the shared-memory rows
+    auto onchip_all = [&](auto full_c) {
+      int il = 0;
+      if constexpr (OO && SDSN_PAIR && decltype(mode_c)::value == SWEEP_PASS) {
+        const int nt = min(NT, non);
+        for (; il + 1 < nt; il += 2) onchip2(full_c, il);
+        if (il < nt) onchip(full_c, il++);
+        for (; il + 1 < non; il += 2) onchip2(full_c, il);
+      }
+      for (; il < non; ++il) onchip(full_c, il);
     };
     // FP32 on-chip rows: the round-1 row body (one register array for TMEM / shared memory /
     // global words; the split body below measured slower for FP32: n = 16384 354 → 436 us/pass)
@@ -419,8 +490,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
       for (int il = 0; il < non; ++il) onchip32(il);
     auto run = [&](auto full_c) {
       constexpr bool FULL = decltype(full_c)::value;
-      if constexpr (kF64Body)
-        for (int il = 0; il < non; ++il) onchip(full_c, il);
+      if constexpr (kF64Body) onchip_all(full_c);
       for (int base = 0; base < nrs; base += PD) {
         T rs[PD];
 #pragma unroll
@@ -677,7 +747,6 @@ int sdsn_grid_for(long n, int num_sms) {
 
 template <typename T, int VPL>
 static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int cg) {
-  auto fn = sdsn_kernel<T, VPL>;
   const int RG = kSdsnWarps / cg;
   const long rows_max = (p.n + grid - 1) / grid + 1;
   size_t dsm = ((sizeof(double) * rows_max * cg + 15) & ~15ul) + (RG > 1 ? (size_t)RG * p.ld * sizeof(T) : 0) +
@@ -696,6 +765,9 @@ static cudaError_t launch_t(const SdsnParams& p, cudaStream_t st, int grid, int 
     nsm = (int)std::max<long>(0, std::min<long>(R - nt, avail / row_bytes));
     dsm += (size_t)nsm * row_bytes;
   }
+  auto fn = sdsn_kernel<T, VPL, false>;
+  if constexpr (sizeof(T) == 8 && VPL <= 4)
+    if (RG == 1 && SDSN_ONCHIP && nt + nsm >= (p.n + grid - 1) / grid) fn = sdsn_kernel<T, VPL, true>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
   if (e != cudaSuccess) return e;
   SdsnParams pp = p;
