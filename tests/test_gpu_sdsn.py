@@ -226,10 +226,12 @@ def test_sdsn_fp32_streaming_gamma_stop():
     assert np.all(Dn >= 0.0)
 
 
-@pytest.mark.parametrize("n", [4100, 6007, 8192])
+@pytest.mark.parametrize("n", [1500, 2047, 2048, 3000, 4100, 6007, 8192])
 def test_sdsn_fp64_streaming_sizes(n):
-    # FP64 above n = 4096: the streaming kernel with 8 vectors per lane (b and the column accumulators
-    # in shared memory), ragged row blocks and an odd column tail (6007); oracle at a fixed pass count.
+    # FP64 K4 plans: the on-chip-only instantiation with paired rows (1500, 2047 ragged, 2048 full),
+    # on-chip + streamed rows (3000), and above n = 4096 the streaming kernel with 8 vectors per lane
+    # (b and the column accumulators in shared memory), ragged row blocks and an odd column tail
+    # (6007); oracle at a fixed pass count.
     X = random_nonneg(_rng(91 + n), n, "sparse")
     k = 5
     h = fram_create(n, schedule=Schedule(theta=10.0, sdsn_fixed=k))

@@ -22,7 +22,8 @@ def _g(x, dt=torch.float64):
 
 
 @pytest.mark.parametrize("n,prec,kernel", [(20, "fp64", 4), (500, "fp64", 4), (64, "fp32", 4), (500, "fp32", 2),
-                                           (2048, "fp32", 2), (4096, "fp32", 2), (4096, "fp64", 1), (5000, "fp32", 1)])
+                                           (2048, "fp32", 2), (4096, "fp32", 2), (2048, "fp64", 1), (4096, "fp64", 1),
+                                           (5000, "fp32", 1)])
 def test_sdsn_repeat_bit_identical(n, prec, kernel, errlog):
     rng = np.random.Generator(np.random.PCG64(n))
     X = random_nonneg(rng, n, "sparse") + 0.1 * np.eye(n)
