@@ -173,7 +173,6 @@ __global__ void __launch_bounds__(BT) fram_batched_kernel(BatchParams P) {
   unsigned char* lused = carve(NP + 1);
   __shared__ double s_scal[4];
   __shared__ unsigned long long s_bad[3];
-  __shared__ int s_flag;
 
   const long inst = blockIdx.x;
   const int n = P.n, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

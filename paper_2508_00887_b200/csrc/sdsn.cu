@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(kSdsnThreads, 1) sdsn_kernel(SdsnParams P, int
           if (rr < nrs) {
             const int il = rg + rmap(rr) * RG;               // local row index
             VT* row = Yc + il * ldv;
-            const T a = (mode == SWEEP_PASS) ? s_a[il] : (T)0;
+            [[maybe_unused]] const T a = (mode == SWEEP_PASS) ? s_a[il] : (T)0;
 #pragma unroll
             for (int k = 0; k < VPL; ++k) {
               if (FULL || kindf(k)) {

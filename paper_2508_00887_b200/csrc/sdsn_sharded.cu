@@ -55,7 +55,6 @@ __global__ void __launch_bounds__(kShThreads, 1) sh_pass_kernel(ShardSdsnParams 
   using VT = typename V4<T>::t;
   constexpr int W = V4<T>::W;
   extern __shared__ __align__(16) unsigned char dsm[];
-  __shared__ double s_w[kShThreads / 32];
   ShardSdsnState* st = P.state;
   if (st->done) return;
   const int p = st->pass;                                        // pass index (mode 1), device-side
