@@ -163,7 +163,9 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
         const long col = (long)t * CPT + 4 * (c0 + c);
         float4 v;
         if (col + 3 < n) {
-          v = __ldcg(reinterpret_cast<const float4*>(grow + col));
+          // L1-allocating: a lane's 16-byte loads of one row are two per 32-byte sector (the column-
+          // owner layout); the second one hits L1 (per call 320 → 300 us, `profiles/r02/ab_k4r_ldca.log`)
+          v = __ldca(reinterpret_cast<const float4*>(grow + col));
         } else {
           v.x = col < n ? grow[col] : 0.f;
           v.y = col + 1 < n ? grow[col + 1] : 0.f;
