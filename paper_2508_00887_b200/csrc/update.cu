@@ -10,6 +10,12 @@
 namespace fram {
 namespace {
 
+#ifndef UPD_V2
+#define UPD_V2 1
+#endif
+#ifndef UPD_OCC
+#define UPD_OCC 1
+#endif
 constexpr int UPD_THREADS = 512;
 
 template <int OP> __device__ __forceinline__ void store_op(void* p, long idx, double v);
@@ -23,6 +29,29 @@ template <> __device__ __forceinline__ void store_op<2>(void* p, long idx, doubl
 template <> __device__ __forceinline__ void store_op<3>(void* p, long idx, double v) {
   reinterpret_cast<__half*>(p)[idx] = __double2half(v);
 }
+
+// two adjacent N_q entries with one store (idx even, ld even)
+template <int OP> __device__ __forceinline__ void store_op2(void* p, long idx, double v0, double v1);
+template <> __device__ __forceinline__ void store_op2<0>(void*, long, double, double) {}
+template <> __device__ __forceinline__ void store_op2<1>(void* p, long idx, double v0, double v1) {
+  *reinterpret_cast<float2*>(reinterpret_cast<float*>(p) + idx) =
+      make_float2(tf32_rne(__double2float_rn(v0)), tf32_rne(__double2float_rn(v1)));
+}
+template <> __device__ __forceinline__ void store_op2<2>(void* p, long idx, double v0, double v1) {
+  __nv_bfloat162 t;
+  t.x = __double2bfloat16(v0);
+  t.y = __double2bfloat16(v1);
+  *reinterpret_cast<__nv_bfloat162*>(reinterpret_cast<__nv_bfloat16*>(p) + idx) = t;
+}
+template <> __device__ __forceinline__ void store_op2<3>(void* p, long idx, double v0, double v1) {
+  __half2 t;
+  t.x = __double2half(v0);
+  t.y = __double2half(v1);
+  *reinterpret_cast<__half2*>(reinterpret_cast<__half*>(p) + idx) = t;
+}
+template <typename TD> struct Pair;
+template <> struct Pair<float> { using t = float2; };
+template <> struct Pair<double> { using t = double2; };
 
 template <int OP, typename TD>
 __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict__ N, const TD* __restrict__ D,
@@ -53,8 +82,14 @@ __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict_
         const long pp = p0 + (long)u * UPD_THREADS;
         if (pp < npair) {
           o[u] = reinterpret_cast<const double2*>(nr)[pp];
-          d0[u] = (double)dr[2 * pp];
-          d1[u] = (double)dr[2 * pp + 1];
+          if constexpr (UPD_V2) {
+            const typename Pair<TD>::t dv = reinterpret_cast<const typename Pair<TD>::t*>(dr)[pp];
+            d0[u] = (double)dv.x;
+            d1[u] = (double)dv.y;
+          } else {
+            d0[u] = (double)dr[2 * pp];
+            d1[u] = (double)dr[2 * pp + 1];
+          }
         }
       }
 #pragma unroll
@@ -65,8 +100,11 @@ __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict_
           upd1(o[u].x, d0[u], nv.x);
           upd1(o[u].y, d1[u], nv.y);
           reinterpret_cast<double2*>(nr)[pp] = nv;
-          store_op<OP>(Nq, i * ld + 2 * pp, nv.x);
-          store_op<OP>(Nq, i * ld + 2 * pp + 1, nv.y);
+          if constexpr (UPD_V2) store_op2<OP>(Nq, i * ld + 2 * pp, nv.x, nv.y);
+          else {
+            store_op<OP>(Nq, i * ld + 2 * pp, nv.x);
+            store_op<OP>(Nq, i * ld + 2 * pp + 1, nv.y);
+          }
         }
       }
     }
@@ -138,15 +176,27 @@ __global__ void copy2d_kernel(double* dst, long ldd, const double* src, long lds
 
 }  // namespace
 
+template <int OP, typename TD>
+static void launch_upd(double* N, const void* D, void* Nq, long rows, long n, long ld, double alpha,
+                       double* partials, unsigned* counter, double* out3, cudaStream_t st, int num_sms) {
+  int per_sm = 4;
+  if (UPD_OCC) {                                       // exactly the resident CTAs: one wave
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<OP, TD>, UPD_THREADS, 0) == cudaSuccess &&
+        occ > 0)
+      per_sm = occ < 4 ? occ : 4;                      // the partials buffer holds 4 CTAs per SM
+  }
+  const int grid = (int)((rows < (long)num_sms * per_sm) ? rows : (long)num_sms * per_sm);
+  update_kernel<OP, TD><<<grid, UPD_THREADS, 0, st>>>(N, (const TD*)D, Nq, rows, n, ld, alpha, partials, counter,
+                                                      out3);
+}
+
 cudaError_t launch_update(double* N, const void* D, bool d_f64, void* Nq, int op, long rows, long n, long ld,
                           double alpha, double* partials, unsigned* counter, double* out3, cudaStream_t st,
                           int num_sms) {
-  const int grid = (int)((rows < (long)num_sms * 4) ? rows : (long)num_sms * 4);
 #define UPD_CASE(OPV)                                                                                        \
-  if (d_f64) update_kernel<OPV, double><<<grid, UPD_THREADS, 0, st>>>(N, (const double*)D, Nq, rows, n, ld, alpha, \
-                                                                    partials, counter, out3);                \
-  else update_kernel<OPV, float><<<grid, UPD_THREADS, 0, st>>>(N, (const float*)D, Nq, rows, n, ld, alpha,         \
-                                                             partials, counter, out3);
+  if (d_f64) launch_upd<OPV, double>(N, D, Nq, rows, n, ld, alpha, partials, counter, out3, st, num_sms);      \
+  else launch_upd<OPV, float>(N, D, Nq, rows, n, ld, alpha, partials, counter, out3, st, num_sms);
   switch (op) {
     case 0: UPD_CASE(0) break;
     case 1: UPD_CASE(1) break;
