@@ -75,6 +75,8 @@ struct fram_ctx {
   DevBuf scan;
   double* hscal = nullptr;          // pinned readback
   cudaEvent_t ev[8] = {};
+  cudaStream_t side = nullptr;                 // X_out copy-out, concurrent with the LAP
+  cudaEvent_t sev[2] = {};
   int64_t launches = 0;
   // batched workspace
   fram::BatchedWs bws;
@@ -198,6 +200,9 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
   if (!h->hscal) CK(cudaMallocHost((void**)&h->hscal, kScalDoubles * 8), "alloc pinned");
   for (auto& e : h->ev)
     if (!e) CK(cudaEventCreate(&e), "event create");
+  if (!h->side) CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "side stream");
+  for (auto& e : h->sev)
+    if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
   return FRAM_OK;
 }
 
@@ -805,6 +810,9 @@ void fram_destroy(fram_handle h) {
   if (h->hscal) cudaFreeHost(h->hscal);
   for (auto& e : h->ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->sev)
+    if (e) cudaEventDestroy(e);
+  if (h->side) cudaStreamDestroy(h->side);
   fram::batched_release(h->bws);
   if (h->shard) fram::shard_destroy(h->shard);
   delete h;
@@ -900,11 +908,17 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     }
   }
   if (t > T) t = T;
+  if (X_out) {                                // N is final: copy it out on the side stream while the LAP runs
+    CK(cudaEventRecord(h->sev[0], st), "event");
+    CK(cudaStreamWaitEvent(h->side, h->sev[0], 0), "side wait");
+    CK(cudaMemcpy2DAsync(X_out, n * 8, h->N.p, ld * 8, n * 8, n, cudaMemcpyDefault, h->side), "X_out copy");
+    CK(cudaEventRecord(h->sev[1], h->side), "event");
+  }
   if (timing) CK(cudaEventRecord(h->ev[6], st), "event");
   CK(fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
   h->launches++;
   if (timing) CK(cudaEventRecord(h->ev[7], st), "event");
-  if (X_out) CK(cudaMemcpy2DAsync(X_out, n * 8, h->N.p, ld * 8, n * 8, n, cudaMemcpyDefault, st), "X_out copy");
+  if (X_out) CK(cudaStreamWaitEvent(st, h->sev[1], 0), "join X_out copy");
   if (perm_out) CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
   CK(cudaStreamSynchronize(st), "final sync");
   if (stats) {

@@ -179,13 +179,15 @@ __global__ void copy2d_kernel(double* dst, long ldd, const double* src, long lds
 template <int OP, typename TD>
 static void launch_upd(double* N, const void* D, void* Nq, long rows, long n, long ld, double alpha,
                        double* partials, unsigned* counter, double* out3, cudaStream_t st, int num_sms) {
-  int per_sm = 4;
-  if (UPD_OCC) {                                       // exactly the resident CTAs: one wave
+  // exactly the resident CTAs: one wave (the partials buffer holds at most 4 CTAs per SM); computed
+  // once per instantiation (thread-safe static initialisation; every device here is an sm_100a B200)
+  static const int per_sm = []() {
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<OP, TD>, UPD_THREADS, 0) == cudaSuccess &&
-        occ > 0)
-      per_sm = occ < 4 ? occ : 4;                      // the partials buffer holds 4 CTAs per SM
-  }
+    if (!UPD_OCC || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<OP, TD>, UPD_THREADS, 0) !=
+                        cudaSuccess || occ <= 0)
+      return 4;
+    return occ < 4 ? occ : 4;
+  }();
   const int grid = (int)((rows < (long)num_sms * per_sm) ? rows : (long)num_sms * per_sm);
   update_kernel<OP, TD><<<grid, UPD_THREADS, 0, st>>>(N, (const TD*)D, Nq, rows, n, ld, alpha, partials, counter,
                                                       out3);
