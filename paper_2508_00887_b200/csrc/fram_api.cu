@@ -915,10 +915,13 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     CK(cudaEventRecord(h->sev[1], h->side), "event");
   }
   if (timing) CK(cudaEventRecord(h->ev[6], st), "event");
-  CK(fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st), "lap");
+  const cudaError_t lap_e = fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st);
+  // join the copy before any return: the next call on `st` rewrites N
+  const cudaError_t join_e = X_out ? cudaStreamWaitEvent(st, h->sev[1], 0) : cudaSuccess;
+  CK(lap_e, "lap");
+  CK(join_e, "join X_out copy");
   h->launches++;
   if (timing) CK(cudaEventRecord(h->ev[7], st), "event");
-  if (X_out) CK(cudaStreamWaitEvent(st, h->sev[1], 0), "join X_out copy");
   if (perm_out) CK(cudaMemcpyAsync(perm_out, h->permd.p, n * 4, cudaMemcpyDefault, st), "perm copy");
   CK(cudaStreamSynchronize(st), "final sync");
   if (stats) {
