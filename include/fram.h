@@ -13,7 +13,8 @@
  *    retains a caller pointer after the call returns.
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every entry
  *    point enqueues its work on `stream` and returns after cudaStreamSynchronize(stream), so
- *    status, outputs and stats are final on return.
+ *    status, outputs and stats are final on return.  (fram_solve copies X_out on a handle-owned
+ *    non-blocking stream while the LAP runs; that copy is joined into `stream` before return.)
  *  - A handle is created for one n and one device; it owns all workspace (allocated lazily on
  *    first use, sized for n).  A handle is not thread-safe; distinct handles are independent.
  *  - On any status other than FRAM_OK / FRAM_NOT_CONVERGED, outputs are left untouched and
