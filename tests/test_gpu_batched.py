@@ -147,3 +147,43 @@ def test_batched_above_64_per_instance_status():
     assert st == FRAM_ERR_DATA
     assert sts[1] == FRAM_ERR_DATA and sts[0] in (FRAM_OK, FRAM_NOT_CONVERGED) and sts[2] in (FRAM_OK, FRAM_NOT_CONVERGED)
     assert sorted(perm[0].cpu().numpy()) == list(range(n))
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("prec", ["fp64", "bf16", "tf32"])
+def test_batched_c3_full_batch_sampled(prec, errlog):
+    # config C3 at its full size (4096 instances of n = 64, the bench's launch configuration), FP32 inputs
+    # as in `bench.py --workload c3`; 16 sampled instances (first, last, spread) vs the oracle's solve of
+    # the same instance: FP64 per-instance N ≤ 1e-9 (one near-threshold pass flip tolerated), mixed modes
+    # the LAP of the GPU's own N bit-exact and accuracy / Φ against the oracle's (north-star tolerances)
+    insts = config_c3_batch(4096)
+    A, B, K = (_g(_stack(insts, a), torch.float32) for a in ("A", "B", "K"))
+    h = fram_create(64, schedule=Schedule(theta=2.0))
+    st, stats, X, perm, sts = fram_solve_batched(h, A, B, K, precision=prec)
+    assert st in (FRAM_OK, FRAM_NOT_CONVERGED) and len(sts) == 4096
+    rng = np.random.Generator(np.random.PCG64(3))
+    sample = sorted(set([0, 1, 4095] + list(rng.choice(4096, size=13, replace=False))))
+    Xs = X[torch.tensor(sample, device="cuda")].cpu().numpy()
+    Ps = perm[torch.tensor(sample, device="cuda")].cpu().numpy()
+    agree, accs, accs_o, rel, worst = 0, [], [], [], 0.0
+    for k, b in enumerate(sample):
+        inst = insts[b]
+        f = lambda M: M.astype(np.float32).astype(np.float64)
+        ref = oracle.fram(f(inst.A), f(inst.B), f(inst.K), theta=2.0)
+        assert np.array_equal(Ps[k], oracle.lap_max(Xs[k]))
+        if prec == "fp64":
+            e = float(np.max(np.abs(Xs[k] - ref["N"])))
+            agree += e <= 1e-9
+            worst = max(worst, e if e <= 1e-9 else 0.0)
+        accs.append(oracle.node_accuracy(Ps[k], inst.perm_true, inst.inlier_mask))
+        accs_o.append(oracle.node_accuracy(ref["perm"], inst.perm_true, inst.inlier_mask))
+        phi = oracle.objective_perm(inst.A, inst.B, inst.K, Ps[k])
+        phi_o = oracle.objective_perm(inst.A, inst.B, inst.K, ref["perm"])
+        rel.append(abs(phi - phi_o) / abs(phi_o))
+    if prec == "fp64":
+        errlog("c3 full batch fp64 max|N-N_oracle| (agreeing instances)", worst, 1e-9, agree=agree, of=len(sample))
+        assert agree >= len(sample) - 1
+    errlog(f"c3 full batch {prec} |dacc|", abs(np.mean(accs) - np.mean(accs_o)), 0.005)
+    errlog(f"c3 full batch {prec} median |dPhi|/Phi", float(np.median(rel)), 1e-3)
+    assert abs(np.mean(accs) - np.mean(accs_o)) <= 0.005
+    assert np.median(rel) <= 1e-3
