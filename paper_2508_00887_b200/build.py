@@ -50,6 +50,9 @@ def _compile(src):
 
 def build(force=False, verbose=False):
     if not force and not needs_build():
+        if os.path.exists(DEMO_SRC) and (not os.path.exists(DEMO_BIN) or
+                                         os.path.getmtime(DEMO_BIN) < max(os.path.getmtime(DEMO_SRC), os.path.getmtime(LIB))):
+            build_demo()
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
@@ -65,7 +68,28 @@ def build(force=False, verbose=False):
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    build_demo()
     return LIB
+
+
+DEMO_SRC = os.path.join(ROOT, "examples", "fram_demo.c")
+DEMO_BIN = os.path.join(ROOT, "examples", "fram_demo")
+
+
+def build_demo():
+    """examples/fram_demo: the C ABI from plain C (gcc, include/fram.h, -lfram with an rpath to the
+    in-tree library).  Skipped without gcc or the source."""
+    if not os.path.exists(DEMO_SRC) or not os.path.exists(LIB):
+        return None
+    cmd = ["gcc", "-O2", "-std=c99", "-Wall", "-I" + os.path.join(ROOT, "include"), DEMO_SRC, "-L" + PKG, "-lfram",
+           "-Wl,-rpath," + PKG, "-o", DEMO_BIN]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True)
+    except FileNotFoundError:
+        return None
+    if r.returncode != 0:
+        raise RuntimeError(f"demo build failed:\n{r.stdout}\n{r.stderr}")
+    return DEMO_BIN
 
 
 if __name__ == "__main__":

@@ -82,3 +82,30 @@ def test_replay_longer_than_max_outer_is_usage_error():
     assert e.value.status == fb.FRAM_ERR_USAGE
     h = fb.fram_create(16, schedule=fb.Schedule(max_outer=4, replay=[5, 5, 5, 5]))
     assert h.schedule.max_outer == 4
+
+
+def test_c_demo_no_cpu_fallback():
+    # examples/fram_demo uses the C ABI from plain C with host buffers; without a GPU the solve must
+    # fail with FRAM_ERR_CUDA (status 4), never fall back to a CPU computation
+    import os
+    import subprocess
+    import torch
+    from paper_2508_00887_b200 import build as b
+    b.build()
+    assert os.path.exists(b.DEMO_BIN)
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present: covered by test_gpu_c_demo")
+    r = subprocess.run([b.DEMO_BIN, "32", "0"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "status 4" in r.stderr, (r.returncode, r.stderr)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("prec", [0, 2])
+def test_gpu_c_demo(prec):
+    # the same C program on the GPU: a noise-free relabelled weighted graph pair is matched exactly
+    import subprocess
+    from paper_2508_00887_b200 import build as b
+    b.build()
+    r = subprocess.run([b.DEMO_BIN, "64", str(prec)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.stdout, r.stderr)
+    assert "accuracy=1.0000" in r.stdout
