@@ -77,6 +77,7 @@ struct fram_ctx {
   cudaEvent_t ev[8] = {};
   cudaStream_t side = nullptr;                 // X_out copy-out, concurrent with the LAP
   cudaEvent_t sev[2] = {};
+  cudaEvent_t gev[3] = {};                     // queued-gradient timing pair (odd iterations), scalar readback
   int64_t launches = 0;
   // batched workspace
   fram::BatchedWs bws;
@@ -203,6 +204,9 @@ fram_status ensure_ws(fram_ctx* h, int op, bool withK) {
   if (!h->side) CK(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking), "side stream");
   for (auto& e : h->sev)
     if (!e) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+  if (!h->gev[0]) CK(cudaEventCreate(&h->gev[0]), "event create");
+  if (!h->gev[1]) CK(cudaEventCreate(&h->gev[1]), "event create");
+  if (!h->gev[2]) CK(cudaEventCreateWithFlags(&h->gev[2], cudaEventDisableTiming), "event create");
   return FRAM_OK;
 }
 
@@ -812,6 +816,8 @@ void fram_destroy(fram_handle h) {
     if (e) cudaEventDestroy(e);
   for (auto& e : h->sev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : h->gev)
+    if (e) cudaEventDestroy(e);
   if (h->side) cudaStreamDestroy(h->side);
   fram::batched_release(h->bws);
   if (h->shard) fram::shard_destroy(h->shard);
@@ -865,10 +871,20 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
   int t = 0, capped = 0;
   int64_t total = 0;
   bool converged = false;
+  // The gradient of iteration t+1 is queued before the host waits for iteration t's scalars (δ, passes):
+  // it reads only N_q, written by update t in stream order, so the GPU runs it while the host reads δ
+  // instead of idling between iterations.  After the last iteration one queued gradient is wasted
+  // (it writes U and G only; the LAP reads N).  Its events alternate between two pairs.
+  auto queue_gradient = [&](int par) -> fram_status {
+    if (timing) CK(cudaEventRecord(par ? h->gev[0] : h->ev[2], st), "event");
+    fram_status r_ = gradient(h, op, dK != nullptr, st);
+    if (r_ != FRAM_OK) return r_;
+    if (timing) CK(cudaEventRecord(par ? h->gev[1] : h->ev[3], st), "event");
+    return FRAM_OK;
+  };
+  if ((rs = queue_gradient(0)) != FRAM_OK) return rs;
   for (t = 1; t <= T; ++t) {
-    if (timing) CK(cudaEventRecord(h->ev[2], st), "event");
-    if ((rs = gradient(h, op, dK != nullptr, st)) != FRAM_OK) return rs;
-    if (timing) CK(cudaEventRecord(h->ev[3], st), "event");
+    const int par = (t - 1) & 1;
     const int fixed = replay ? h->replay[t - 1] : sc.sdsn_fixed;
     if ((rs = run_sdsn(h, f64, fixed, st)) != FRAM_OK) return rs;
     if (timing) CK(cudaEventRecord(h->ev[4], st), "event");
@@ -879,7 +895,9 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     h->launches++;
     if (timing) CK(cudaEventRecord(h->ev[5], st), "event");
     CK(cudaMemcpyAsync(h->hscal, scal, kScalDoubles * 8, cudaMemcpyDeviceToHost, st), "scalar readback");
-    CK(cudaStreamSynchronize(st), "iteration sync");
+    CK(cudaEventRecord(h->gev[2], st), "event");
+    if (t < T && (rs = queue_gradient(par ^ 1)) != FRAM_OK) return rs;
+    CK(cudaEventSynchronize(h->gev[2]), "iteration sync");
     const int passes = *reinterpret_cast<int*>(h->hscal + 8);
     const double gam = h->hscal[0];
     const double delta = h->hscal[6];
@@ -888,8 +906,9 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     if (fixed == 0 && passes >= sc.sdsn_max) ++capped;
     if (timing) {
       float a, b, cc;
-      cudaEventElapsedTime(&a, h->ev[2], h->ev[3]);
-      cudaEventElapsedTime(&b, h->ev[3], h->ev[4]);
+      cudaEvent_t g0 = par ? h->gev[0] : h->ev[2], g1 = par ? h->gev[1] : h->ev[3];
+      cudaEventElapsedTime(&a, g0, g1);
+      cudaEventElapsedTime(&b, g1, h->ev[4]);
       cudaEventElapsedTime(&cc, h->ev[4], h->ev[5]);
       ms_gemm += a;
       ms_sdsn += b;
