@@ -9,23 +9,11 @@
 namespace fram {
 namespace {
 
-#ifndef GF_TM
-#define GF_TM 64
-#endif
-#ifndef GF_TN
-#define GF_TN 64
-#endif
-#ifndef GF_TK
-#define GF_TK 16
-#endif
-#ifndef GF_NS
-#define GF_NS 2
-#endif
-#ifndef GF_PAD
-#define GF_PAD 4
-#endif
 // CTA tile TM×TN, k-slab TK, NS-stage cp.async ring; one warp per 32×32 sub-tile (4×4 DMMA 8×8×4).
-constexpr int TM = GF_TM, TN = GF_TN, TK = GF_TK, NS = GF_NS, PADK = TK + GF_PAD;
+// Shared-memory row pitch TK + 4 doubles (≡ 8 words mod 32: conflict-free fragment loads).  Measured
+// alternatives (profiles/r02/ab_dmma.log): NS = 3 / 4, 128×64 and 128×128 tiles, TK = 32 — equal or
+// slower (the DMMA pipe is ~90% busy).
+constexpr int TM = 64, TN = 64, TK = 16, NS = 2, PADK = TK + 4;
 constexpr int THREADS = (TM / 32) * (TN / 32) * 32;
 constexpr size_t SMEM = (size_t)NS * (TM + TN) * PADK * sizeof(double);
 

@@ -10,12 +10,6 @@
 namespace fram {
 namespace {
 
-#ifndef UPD_V2
-#define UPD_V2 1
-#endif
-#ifndef UPD_OCC
-#define UPD_OCC 1
-#endif
 constexpr int UPD_THREADS = 512;
 
 template <int OP> __device__ __forceinline__ void store_op(void* p, long idx, double v);
@@ -82,14 +76,9 @@ __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict_
         const long pp = p0 + (long)u * UPD_THREADS;
         if (pp < npair) {
           o[u] = reinterpret_cast<const double2*>(nr)[pp];
-          if constexpr (UPD_V2) {
-            const typename Pair<TD>::t dv = reinterpret_cast<const typename Pair<TD>::t*>(dr)[pp];
-            d0[u] = (double)dv.x;
-            d1[u] = (double)dv.y;
-          } else {
-            d0[u] = (double)dr[2 * pp];
-            d1[u] = (double)dr[2 * pp + 1];
-          }
+          const typename Pair<TD>::t dv = reinterpret_cast<const typename Pair<TD>::t*>(dr)[pp];
+          d0[u] = (double)dv.x;
+          d1[u] = (double)dv.y;
         }
       }
 #pragma unroll
@@ -100,11 +89,7 @@ __global__ void __launch_bounds__(UPD_THREADS) update_kernel(double* __restrict_
           upd1(o[u].x, d0[u], nv.x);
           upd1(o[u].y, d1[u], nv.y);
           reinterpret_cast<double2*>(nr)[pp] = nv;
-          if constexpr (UPD_V2) store_op2<OP>(Nq, i * ld + 2 * pp, nv.x, nv.y);
-          else {
-            store_op<OP>(Nq, i * ld + 2 * pp, nv.x);
-            store_op<OP>(Nq, i * ld + 2 * pp + 1, nv.y);
-          }
+          store_op2<OP>(Nq, i * ld + 2 * pp, nv.x, nv.y);
         }
       }
     }
@@ -183,7 +168,7 @@ static void launch_upd(double* N, const void* D, void* Nq, long rows, long n, lo
   // once per instantiation (thread-safe static initialisation; every device here is an sm_100a B200)
   static const int per_sm = []() {
     int occ = 0;
-    if (!UPD_OCC || cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<OP, TD>, UPD_THREADS, 0) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<OP, TD>, UPD_THREADS, 0) !=
                         cudaSuccess || occ <= 0)
       return 4;
     return occ < 4 ? occ : 4;
