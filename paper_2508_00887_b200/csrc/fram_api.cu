@@ -15,6 +15,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/fram.h"
 #include "internal.h"
 #include "batched.h"
@@ -54,6 +56,15 @@ size_t op_size(int op) { return op == 0 ? 8 : (op == 1 ? 4 : 2); }
 size_t dt_size(int dt) { return dt == 0 ? 8 : (dt == 1 ? 4 : 2); }
 
 }  // namespace
+
+// NVTX ranges (header-only NVTX v3: no library, ~ns per range when no tool is attached) around a solve
+// and its phases, for ncu --nvtx / nsys timelines.  Host-side: they mark when the work is enqueued.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 struct fram_ctx {
   int64_t n = 0;
@@ -414,6 +425,7 @@ fram_status common_checks(fram_ctx* h, int dt, fram_precision p) {
 // and every rank runs the same deterministic LAP (identical perm everywhere).
 fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, const void* K, const double* X0,
                           int op, cudaStream_t st, double* X_out, int32_t* perm_out, fram_stats* stats) {
+  NvtxRange range_("sharded_solve");
   fram::ShardCtx* sh = h->shard;
   const int W = fram::shard_world(sh);
   const long n = h->n, m = n / W, ld = h->ld;
@@ -648,6 +660,7 @@ fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, con
 // served by the group (sharded.cu).  Rank 0 writes perm_out and the stats.
 fram_status group_solve(fram_ctx* g, int dt, const void* A, const void* B, const void* K, const double* X0, int op,
                         cudaStream_t caller, double* X_out, int32_t* perm_out, fram_stats* stats) {
+  NvtxRange range_("group_solve");
   const int W = (int)g->vsub.size();
   const long n = g->n, m = n / W;
   CK(cudaStreamSynchronize(caller), "caller stream sync");        // inputs produced on the caller's stream
@@ -830,6 +843,7 @@ const char* fram_build_info(void) { return "libfram sm_100a (tcgen05/TMEM/TMA GE
 
 fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* B, const void* K, const double* X0,
                        fram_precision p, void* stream, double* X_out, int32_t* perm_out, fram_stats* stats) {
+  NvtxRange range_solve("fram_solve");
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (!A || !B) return fail(FRAM_ERR_USAGE, "A and B are required");
@@ -858,7 +872,10 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
   if ((rs = stage_in(h, h->stX0, X0, (size_t)n * n * 8, st, &dX0)) != FRAM_OK) return rs;
 
   double c = 0;
-  if ((rs = precondition(h, (int)dt, dA, dB, dK, op, st, &c)) != FRAM_OK) return rs;
+  {
+    NvtxRange r_("precondition");
+    if ((rs = precondition(h, (int)dt, dA, dB, dK, op, st, &c)) != FRAM_OK) return rs;
+  }
   CK(fram::launch_init_n(h->N.as<double>(), h->Nq.p, op, (const double*)dX0, n, n, ld, st), "init N");
   h->launches++;
   if (timing) CK(cudaEventRecord(h->ev[1], st), "event");
@@ -876,6 +893,7 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
   // instead of idling between iterations.  After the last iteration one queued gradient is wasted
   // (it writes U and G only; the LAP reads N).  Its events alternate between two pairs.
   auto queue_gradient = [&](int par) -> fram_status {
+    NvtxRange range_("gradient");
     if (timing) CK(cudaEventRecord(par ? h->gev[0] : h->ev[2], st), "event");
     fram_status r_ = gradient(h, op, dK != nullptr, st);
     if (r_ != FRAM_OK) return r_;
@@ -884,9 +902,13 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
   };
   if ((rs = queue_gradient(0)) != FRAM_OK) return rs;
   for (t = 1; t <= T; ++t) {
+    NvtxRange r_outer("outer_iteration");
     const int par = (t - 1) & 1;
     const int fixed = replay ? h->replay[t - 1] : sc.sdsn_fixed;
-    if ((rs = run_sdsn(h, f64, fixed, st)) != FRAM_OK) return rs;
+    {
+      NvtxRange r_("sdsn");
+      if ((rs = run_sdsn(h, f64, fixed, st)) != FRAM_OK) return rs;
+    }
     if (timing) CK(cudaEventRecord(h->ev[4], st), "event");
     CK(fram::launch_update(h->N.as<double>(), h->Y.p, f64, h->Nq.p, op, n, n, ld, sc.alpha, h->upd.as<double>(),
                            reinterpret_cast<unsigned*>(h->upd.as<double>() + h->num_sms * 8 + 8), scal + 4, st,
@@ -934,6 +956,7 @@ fram_status fram_solve(fram_handle h, fram_dtype dt, const void* A, const void* 
     CK(cudaEventRecord(h->sev[1], h->side), "event");
   }
   if (timing) CK(cudaEventRecord(h->ev[6], st), "event");
+  NvtxRange r_lap("lap");
   const cudaError_t lap_e = fram::launch_lap(h->N.as<double>(), n, ld, h->permd.as<int32_t>(), h->lapw.p, st);
   // join the copy before any return: the next call on `st` rewrites N
   const cudaError_t join_e = X_out ? cudaStreamWaitEvent(st, h->sev[1], 0) : cudaSuccess;
@@ -1068,6 +1091,7 @@ fram_status fram_lap(fram_handle h, const double* Nin, int32_t* perm_out, void* 
 fram_status fram_solve_batched(fram_handle h, int64_t batch, fram_dtype dt, const void* A, const void* B,
                                const void* K, const double* X0, fram_precision p, void* stream, double* X_out,
                                int32_t* perm_out, int32_t* status_out, fram_stats* stats) {
+  NvtxRange range_("fram_solve_batched");
   fram_status s0 = common_checks(h, (int)dt, p);
   if (s0 != FRAM_OK) return s0;
   if (batch < 0 || !A || !B) return fail(FRAM_ERR_USAGE, "bad batch arguments");
