@@ -99,7 +99,7 @@ struct fram_ctx {
   std::vector<fram_ctx*> vsub;
   std::vector<cudaStream_t> vstreams;
   fram::VGroup* vgroup = nullptr;
-  // sharded SDSN: a chunk of passes (pass kernel, reduce, finish, all-reduce) captured once as a CUDA
+  // sharded SDSN: a chunk of passes (pass kernel, reduce, all-reduce) captured once as a CUDA
   // graph and relaunched (NCCL communicators only; see sharded_solve)
   cudaGraphExec_t sh_graph = nullptr;
   cudaStream_t sh_cap_stream = nullptr;
@@ -532,12 +532,12 @@ fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, con
     CK(fram::prepare_sdsn_sh(sp, f64, h->num_sms), "sdsn prepare");
     CK(fram::launch_sdsn_sh_sweep(sp, f64, 0, st, h->num_sms), "sdsn scale");
     if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK) return FRAM_ERR_NCCL;
-    h->launches += 5;
+    h->launches += 3;                                  // max, scale sweep, reduce
     const int cap = std::max(1, sp.sdsn_fixed > 0 ? sp.sdsn_fixed : sch.sdsn_max);
     // Passes are queued kChunk at a time between host polls of `done` (passes after the last are no-ops).
     // Every pass is the same launch sequence (the pass index lives on the device), so with an NCCL
     // communicator a chunk is captured once as a CUDA graph — kernels and ncclAllReduce — and relaunched:
-    // one host call per chunk instead of 4 per pass.  Virtual shards synchronise their collectives on
+    // one host call per chunk instead of 3 per pass.  Virtual shards synchronise their collectives on
     // the host and keep the plain launches.
     constexpr int kChunk = 16;
     bool use_graph = !fram::shard_is_virtual(sh) && !h->sh_graph_off;
@@ -573,13 +573,13 @@ fram_status sharded_solve(fram_ctx* h, int dt, const void* A, const void* B, con
     for (int p0 = 0; p0 < cap; p0 += kChunk) {
       if (use_graph) {
         CK(cudaGraphLaunch(h->sh_graph, st), "graph launch");
-        h->launches += 3 * kChunk;
+        h->launches += 2 * kChunk;
       } else {
         for (int p = p0; p < std::min(cap, p0 + kChunk); ++p) {
           CK(fram::launch_sdsn_sh_sweep(sp, f64, 1, st, h->num_sms), "sdsn pass");
           if (nck(fram::shard_allreduce_f64(sh, sp.send, sp.recv, n + 1, false, st, &err)) != FRAM_OK)
             return FRAM_ERR_NCCL;
-          h->launches += 3;
+          h->launches += 2;
         }
       }
       CK(cudaMemcpyAsync(&hstate, sp.state, sizeof(hstate), cudaMemcpyDeviceToHost, st), "state readback");

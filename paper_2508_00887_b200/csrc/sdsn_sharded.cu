@@ -183,10 +183,12 @@ __global__ void __launch_bounds__(kShThreads, 1) sh_pass_kernel(ShardSdsnParams 
   }
 }
 
-// c_j = Σ_CTA partials (FP64, CTA order), S_local = Σ_i r_i → send[0..n]; also promotes
-// done_pending → done (so the reduce/all-reduce of the final pass still runs harmlessly).
+// c_j = Σ_CTA partials (FP64, CTA order), S_local = Σ_i r_i → send[0..n]; then thread 0 of CTA 0
+// advances the pass index (mode 1) and promotes done_pending → done for the next pass kernel (the
+// all-reduce of the final pass still runs, harmlessly).  Another CTA of this kernel may then see done
+// and skip its columns: only after the last pass, whose sums nothing reads.
 template <typename T>
-__global__ void sh_reduce_kernel(ShardSdsnParams P, int nctas) {
+__global__ void sh_reduce_kernel(ShardSdsnParams P, int nctas, int mode) {
   ShardSdsnState* st = P.state;
   if (st->done) return;
   const long n = P.n, ld = P.ld;
@@ -207,14 +209,10 @@ __global__ void sh_reduce_kernel(ShardSdsnParams P, int nctas) {
       double t = 0.0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_w[w];
       P.send[n] = t;
+      if (st->done_pending) st->done = 1;
+      if (mode == 1) st->pass += 1;
     }
   }
-}
-
-__global__ void sh_finish_kernel(ShardSdsnState* st, int mode) {
-  if (st->done) return;
-  if (st->done_pending) st->done = 1;
-  if (mode == 1) st->pass += 1;
 }
 
 }  // namespace
@@ -252,12 +250,11 @@ cudaError_t launch_sdsn_sh_sweep(const ShardSdsnParams& p, bool f64, int mode, c
   const size_t sm = sdsn_sh_smem(p.ld, f64, (p.rows + g - 1) / g + 1);
   if (f64) {
     sh_pass_kernel<double><<<g, kShThreads, sm, st>>>(p, mode);
-    sh_reduce_kernel<double><<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(p, g);
+    sh_reduce_kernel<double><<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(p, g, mode);
   } else {
     sh_pass_kernel<float><<<g, kShThreads, sm, st>>>(p, mode);
-    sh_reduce_kernel<float><<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(p, g);
+    sh_reduce_kernel<float><<<(unsigned)((p.n + 255) / 256), 256, 0, st>>>(p, g, mode);
   }
-  sh_finish_kernel<<<1, 1, 0, st>>>(p.state, mode);
   return cudaGetLastError();
 }
 
