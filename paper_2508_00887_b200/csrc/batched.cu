@@ -519,6 +519,10 @@ cudaError_t launch_b(const BatchParams& p, cudaStream_t st) {
   auto fn = fram_batched_kernel<OP>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
+  // the whole unified L1 as shared memory, so the 2 CTAs per SM the kernel is sized for always fit (left
+  // to the driver, the carveout — and C3 TF32 throughput — varied between runs: 107K vs 137K inst/s)
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+  if (e != cudaSuccess) return e;
   fn<<<(unsigned)p.batch, BT, sm, st>>>(p);
   return cudaGetLastError();
 }

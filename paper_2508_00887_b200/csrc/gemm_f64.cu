@@ -126,8 +126,11 @@ __global__ void __launch_bounds__(THREADS) gemm_f64_kernel(const double* __restr
 }  // namespace
 
 cudaError_t launch_gemm_f64(const GemmArgs& g, cudaStream_t st) {
-  const cudaError_t attr =
-      cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  cudaError_t attr = cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM);
+  // 4 CTAs per SM (register-limited) need 4 × 41 KB of shared memory: ask for the full carveout
+  if (attr == cudaSuccess)
+    attr = cudaFuncSetAttribute(gemm_f64_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared);
   if (attr != cudaSuccess) return attr;
   dim3 grid((unsigned)((g.N + TN - 1) / TN), (unsigned)((g.M + TM - 1) / TM));
   gemm_f64_kernel<<<grid, THREADS, SMEM, st>>>((const double*)g.Aop, (const double*)g.Bop, g.M, g.N, g.K, g.ld, g.epi,
