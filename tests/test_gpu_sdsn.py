@@ -177,7 +177,7 @@ def test_sdsn_deterministic():
     assert k1 == k2 and torch.equal(D1, D2)
 
 
-@pytest.mark.parametrize("n", [33, 129, 777, 1500, 2048, 3000, 4096])
+@pytest.mark.parametrize("n", [33, 129, 777, 1500, 2048, 2049, 2350, 3000, 3001, 4095, 4096])
 def test_sdsn_fp32_onchip_sizes(n, errlog):
     # FP32 SDSN at the sizes that select each on-chip layout (K4r: 4/8/16/32 columns per owner
     # thread, rows in TMEM only or TMEM + shared memory, ragged column tails), a fixed pass count
