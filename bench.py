@@ -22,6 +22,29 @@ import statistics
 import subprocess
 import sys
 import threading
+
+# stdout carries exactly one JSON line per run.  Native libraries print to fd 1 on their own (NCCL
+# prints its "NCCL version" banner under NCCL_DEBUG=VERSION straight to stdout), so while the bench runs
+# fd 1 points at stderr and the JSON line is written to the saved original stdout (emit()).
+_JSON_FD = None
+
+
+def _claim_stdout():
+    global _JSON_FD
+    if _JSON_FD is None:
+        sys.stdout.flush()
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(line):
+    """Write the run's JSON line to the real stdout."""
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -245,7 +268,7 @@ def run_reference(args):
             "config": {"workload": workload(args.precision), "n": args.n, "schedule": SCHEDULE, "seed": 0},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -470,7 +493,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_entry(inst, passes / iters, budget_s=15.0)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -546,7 +569,7 @@ def run_c5(args):
                 "gemm_ms_per_iter": sum(s["ms_gemm"] for s in stats) / max(iters, 1),
                 "lap_ms_per_step": sum(s["ms_lap"] for s in stats) / args.steps,
                 "gpu_launches": sum(s["kernel_launches"] for s in stats), "clocks": clocks}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -623,7 +646,7 @@ def run_c3(args):
                              "note": "SDSN-pass shared-memory bytes only (GEMMs, update, LAP excluded); the kernel is "
                                      "latency / barrier bound at 2 CTAs per SM (DESIGN.md section 10)"},
                 "inlier_accuracy_rank0": acc, "gpu_launches": args.steps, "clocks": clocks}
-        print(json.dumps(line), flush=True)
+        emit(line)
     if world > 1:
         dist.destroy_process_group()
     return 0
@@ -693,12 +716,13 @@ def run_ubc(args):
             "mixed": main, "fp64": res["fp64"],
             "fp64_over_mixed_time_to_solution": res["fp64"]["time_to_solution_ms"] / main["time_to_solution_ms"],
             "paper_context": "12.7x mixed over GPU-FP64 on an RTX 4080 SUPER (P:551), whose FP64 rate is 1/64 of FP32"}
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
 def main():
     args = parse()
+    _claim_stdout()
     if args.impl == "reference":
         return run_reference(args)
     if args.workload == "c5":
