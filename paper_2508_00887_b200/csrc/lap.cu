@@ -346,9 +346,13 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
         if (kr < dkey || (kr == dkey && (int)rr.z < j1)) { dkey = kr; j1 = (int)rr.z; wy1 = (int)rr.w; }
       }
       const int mine = j1;
+      // the row owning this lane's candidate column, loaded while the argmin reduces (p is fixed
+      // during a search), so the winner's row index needs no dependent load after the reduction
+      const int pl = (mine >= 1 && mine <= n) ? p[mine] : 0;
       warp_argmin(dkey, j1);
       const unsigned who = __ballot_sync(0xffffffffu, mine == j1);
       wy1 = __shfl_sync(0xffffffffu, wy1, __ffs(who) - 1);
+      const int pwin = __shfl_sync(0xffffffffu, pl, __ffs(who) - 1);
       const double delta = unkey(dkey);
       ++step;
       if (j1 > n) {                                   // no finite candidate (non-finite N): give up cleanly
@@ -356,7 +360,7 @@ __global__ void __launch_bounds__(THREADS, 1) lap_cluster_kernel(const double* _
         return;                                       // every CTA reduced the same records: all return
       }
       if (tid == 0) { pw[j1] = wy1; dh[ntree] = delta; }   // way of the entering column (final); δ_s, s = ntree
-      const int i0n = p[j1];
+      const int i0n = pwin;                           // = p[j1]
       if (i0n != 0) load_row(i0n);
       const uint32_t usd = inr & ~fr;
 #pragma unroll
