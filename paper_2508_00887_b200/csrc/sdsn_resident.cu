@@ -500,7 +500,10 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
         const double cs = v[0];
         const int f = s >> 2, e4 = s & 3, c = f >> 7, tt = f & 127;
         const long colj = (long)tt * CPT + 4 * c + e4;
-        st_w(P.bvec + s, ptag(colj < n ? (float)(cs / dn) : CUDART_INF_F, e));   // |b_j| = c_j/n
+        // |b_j| = c_j/n by the one-FMA correction of the correctly rounded reciprocal (= the IEEE quotient,
+        // see div_n): the FP64 division left the critical path of every pass (n = 4096: 6.25 → 6.19 µs,
+        // profiles/r02/ab_k4r_bdiv.log; an earlier version of the kernel had measured no gain)
+        st_w(P.bvec + s, ptag(colj < n ? (float)div_n(cs, dn, rn) : CUDART_INF_F, e));
       }
       if (sb + 32 < s1) __syncthreads();               // s_red2 is reused by the next chunk
     }
