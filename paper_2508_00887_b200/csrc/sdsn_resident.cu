@@ -156,9 +156,13 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
   // ---------------- phase L: X rows → on-chip, m = max X (Alg.2 step 1) ----------------
   {
     float lmax = 0.f;
-    for (int r = g; r < R; r += 2) {
+    // 4 rows of loads in flight per row group before their stores (tcgen05.st is an asm with a memory
+    // clobber, so the compiler cannot hoist the next row's loads above it by itself).  The per-call time
+    // did not move, but the pass loop of this build measured 0.5-1% faster at n = 4096
+    // (profiles/r02/ab_k4r_loadrows.log; 2 rows: no change)
+    constexpr int LB = 4;
+    auto load_g = [&](int r, float (&x)[CH]) {
       const float* grow = P.Y + (r0 + r) * ld;
-      float x[CH];
 #pragma unroll
       for (int c = 0; c < VH; ++c) {
         const long col = (long)t * CPT + 4 * (c0 + c);
@@ -174,9 +178,21 @@ __global__ void __launch_bounds__(RK<CPT>::THREADS, 1) sdsn_res_kernel(ResParams
           v.w = col + 3 < n ? grow[col + 3] : 0.f;
         }
         x[4 * c] = v.x; x[4 * c + 1] = v.y; x[4 * c + 2] = v.z; x[4 * c + 3] = v.w;
-        lmax = fmaxf(lmax, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
       }
-      store_row(r, x);
+    };
+    for (int r = g; r < R; r += 2 * LB) {
+      float x[LB][CH];
+#pragma unroll
+      for (int i = 0; i < LB; ++i)
+        if (r + 2 * i < R) load_g(r + 2 * i, x[i]);
+#pragma unroll
+      for (int i = 0; i < LB; ++i) {
+        if (r + 2 * i < R) {
+#pragma unroll
+          for (int k = 0; k < CH; ++k) lmax = fmaxf(lmax, x[i][k]);
+          store_row(r + 2 * i, x[i]);
+        }
+      }
     }
     tmem_wait_st();
     double m = (double)lmax;
