@@ -23,6 +23,8 @@ import subprocess
 import sys
 import threading
 
+import time
+
 # stdout carries exactly one JSON line per run.  Native libraries print to fd 1 on their own (NCCL
 # prints its "NCCL version" banner under NCCL_DEBUG=VERSION straight to stdout), so while the bench runs
 # fd 1 points at stderr and the JSON line is written to the saved original stdout (emit()).
@@ -45,7 +47,6 @@ def emit(line):
         sys.stdout.flush()
     else:
         os.write(_JSON_FD, data)
-import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
