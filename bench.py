@@ -22,7 +22,6 @@ import statistics
 import subprocess
 import sys
 import threading
-
 import time
 
 # stdout carries exactly one JSON line per run.  Native libraries print to fd 1 on their own (NCCL
